@@ -1,0 +1,150 @@
+/*
+ * hc.h — C-ABI of the B200-native Hash Chain (HC) exact string matcher.
+ *
+ * Method: Palmer, Faro, Scafiti, "Efficient Online String Matching through
+ * Linked Weak Factors", arXiv 2310.15711.  P:n = line n of PAPER.md,
+ * S:n = line n of SPEC.md (interfaces and contracts only).
+ *
+ * Problem: find all occurrences of a pattern x of length m in a text y
+ * of length n.  hc_prepare() is the paper's Preprocessing(x, m, q, alpha)
+ * (Fig. 3); hc_search() is the searching phase of HC(x, m, y, n,
+ * q, alpha) (Fig. 5) run on one B200 (sm_100a).
+ *
+ * Result semantics: exactly { s in [0, n-m] : y[s..s+m-1] == x }, ascending,
+ * overlaps included, no duplicates.  HC is an exact
+ * matcher: the filter only rejects windows that cannot hold x
+ * and every survivor is verified byte by byte, so the set does not
+ * depend on q or alpha.  Positions are reported at the window start e-m+1
+ * (reading R1).
+ *
+ * Conventions
+ *   - All functions are extern "C" and thread-safe.  A handle is immutable
+ *     after hc_prepare(): concurrent hc_search() calls on one handle (on any
+ *     streams, from any host threads) are safe.
+ *   - Errors: functions returning int / int64_t return a negative hc_status on
+ *     failure; hc_prepare() returns NULL.  The code of the last failure on the
+ *     calling host thread is available from hc_last_error().
+ *   - Bytes are raw unsigned 0..255; no alphabet mapping.
+ *   - The word width of F is w = 32 (reading R2).
+ */
+#ifndef HC_H_
+#define HC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h> /* cudaStream_t */
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hc_status {
+    HC_OK = 0,
+    HC_EINVAL = -1,    /* NULL x with m > 0, m == 0, q < 1, NULL handle, NULL y with n > 0 */
+    HC_ETOOSHORT = -2, /* q > m */
+    HC_EALPHA = -3,    /* alpha outside [1, 15]: F = 2^alpha 32-bit words must fit in shared memory */
+    HC_ENOMEM = -4,    /* host or device allocation failed */
+    HC_ECUDA = -5,     /* a CUDA runtime call failed (see hc_strerror / stderr) */
+    HC_ETOOLONG = -6,  /* n > HC_MAX_TEXT or m > HC_MAX_PATTERN */
+    HC_ENODEV = -7     /* no CUDA device / device is not sm_100 */
+} hc_status;
+
+#define HC_WORD_BITS 32                  /* w */
+#define HC_MAX_ALPHA 15
+#define HC_MAX_PATTERN 65536u            /* m: x and F are kept in shared memory */
+#define HC_MAX_TEXT 0xFFFF0000ull        /* n: positions are 32-bit inside the kernels */
+
+typedef struct hc_handle hc_handle;
+
+/* Preprocessing(x, m, q, alpha) — Fig. 3, Eq. 1-5.
+ *   x     : HOST pointer to the m pattern bytes; copied, the caller keeps ownership.
+ *   m     : pattern length, 1 <= m <= HC_MAX_PATTERN.
+ *   q     : q-gram length, 1 <= q <= min(m, 8).  (q > m -> HC_ETOOSHORT; q > 8 -> HC_EINVAL.)
+ *   alpha : F has 2^alpha words, 1 <= alpha <= 15; s = floor(alpha/q) (Eq. 4).
+ * Builds F (w = 32) and H_v on the host in Fig. 3 order (including optimisation 1,
+ * P:330-335) and uploads F and x synchronously to the CURRENT device.
+ * Returns a new handle (free with hc_destroy) or NULL (see hc_last_error()). */
+hc_handle *hc_prepare(const uint8_t *x, size_t m, int q, int alpha);
+
+/* Code of the last failure on this host thread (HC_OK if none). */
+int hc_last_error(void);
+
+/* Static description of a status code (never NULL). */
+const char *hc_strerror(int code);
+
+/* Searching phase of HC (Fig. 5 left) on the device.
+ *   y_dev   : DEVICE pointer to the n text bytes; caller-owned, any alignment, never written.
+ *   n       : text length; n < m (including n == 0) returns 0, not an error.
+ *   pos_out : DEVICE pointer to int64_t[max_out], caller-owned; receives the min(count, max_out)
+ *             SMALLEST occurrence start positions, ascending.  NULL or max_out == 0: count only.
+ *   stream  : all device work is enqueued on this stream (ordered after the caller's fill of
+ *             y_dev).  The call returns once the count is known (it synchronises on the count
+ *             read-back); the writes to pos_out are enqueued on `stream` and complete in
+ *             stream order.
+ * Returns the total number of occurrences (>= 0), or a negative hc_status. */
+int64_t hc_search(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t *pos_out,
+                  size_t max_out, cudaStream_t stream);
+
+/* Tuning knobs and statistics for hc_search_ex (tests and the benchmark). */
+typedef enum hc_path {
+    HC_PATH_AUTO = 0,   /* chosen from m, q */
+    HC_PATH_STAGED = 1, /* text tiles staged in shared memory by TMA bulk copies */
+    HC_PATH_GATHER = 2  /* no staging: lanes read only the q-grams they hash, from global memory */
+} hc_path;
+
+typedef struct hc_search_opts {
+    int path;         /* hc_path */
+    int tile_bytes;   /* staged: text bytes per shared-memory stage (0 = default) */
+    int stages;       /* staged: TMA pipeline depth (0 = default) */
+    int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
+    int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
+    int time_kernel;  /* 1: record CUDA events around the search kernel (stats->kernel_ms) */
+} hc_search_opts;
+
+typedef struct hc_search_stats {
+    int path;          /* path used */
+    int grid;          /* CTAs launched by the search kernel */
+    int block;         /* threads per CTA */
+    int smem_bytes;    /* dynamic shared memory per CTA */
+    int64_t tiles;     /* staged: text tiles; gather: lane chunks */
+    int launches;      /* kernels launched by this call (search, re-run, sort, copy) */
+    int reruns;        /* search re-runs after the position scratch overflowed */
+    float kernel_ms;   /* search kernel time (first launch), if time_kernel */
+} hc_search_stats;
+
+/* hc_search with explicit options (NULL = defaults) and optional statistics (NULL = none). */
+int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t *pos_out,
+                     size_t max_out, cudaStream_t stream, const hc_search_opts *opts,
+                     hc_search_stats *stats);
+
+/* End-to-end convenience: y_host and pos_out_host are HOST pointers.  Copies y to the
+ * device (staged through pinned buffers when y_host is pageable), searches, and copies
+ * min(count, max_out) positions back.  Synchronous.  Returns the count or a negative
+ * hc_status. */
+int64_t hc_search_host(const hc_handle *h, const uint8_t *y_host, size_t n,
+                       int64_t *pos_out_host, size_t max_out, cudaStream_t stream);
+
+/* Frees the handle's host and device state.  No search on the handle may be in flight. */
+void hc_destroy(hc_handle *h);
+
+/* Test introspection: the handle's host copy of the table the kernels use.
+ *   *F receives a pointer to 2^alpha uint32_t words owned by the handle (valid until
+ *   hc_destroy); alpha, s (Eq. 4), w (= 32) and H_v are written when non-NULL.
+ * Returns HC_OK or HC_EINVAL. */
+int hc_table(const hc_handle *h, const uint32_t **F, int *alpha, int *s, int *w,
+             uint32_t *h_v);
+
+/* Host-only Preprocessing (no device needed): the same table hc_prepare builds.
+ *   F_out : HOST uint32_t[2^alpha], written in full.  s_out, hv_out: written when non-NULL.
+ * Returns HC_OK or a negative hc_status (same parameter checks as hc_prepare). */
+int hc_build_table(const uint8_t *x, size_t m, int q, int alpha, uint32_t *F_out,
+                   int *s_out, uint32_t *hv_out);
+
+/* Library version string. */
+const char *hc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HC_H_ */

@@ -1,0 +1,408 @@
+// hc_api.cpp — host side of libhc: the C-ABI of include/hc.h.
+//
+//   hc_prepare     Preprocessing (Fig. 3) on the host + upload of F and x.
+//   hc_search(_ex) validation, path choice, search kernel launch (hc_kernels.cu),
+//                  count read-back, position ordering.
+//
+// The table build below is this library's own implementation of Fig. 3: it
+// hashes every q-gram of x once (closed form of Eq. 3, reading R4), applies
+// Eq. 1 to every adjacent non-overlapping pair (the pairs the chains of Fig. 3
+// visit), then Eq. 2 with optimisation 1, and takes H_v
+// as the hash of the first q-gram of the chain ending at m-1.  It
+// shares no code with oracle/; tests check the two tables are identical.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "hc.h"
+#include "hc_internal.h"
+
+struct hc_handle {
+    std::vector<uint8_t> x;
+    std::vector<uint32_t> F;
+    uint32_t m = 0, q = 0, alpha = 0, s = 0, mask = 0, hv = 0;
+    int device = 0;
+    uint32_t *dF = nullptr;
+    uint8_t *dx = nullptr;
+};
+
+namespace {
+
+thread_local int g_last_error = HC_OK;
+
+int fail(int code) {
+    g_last_error = code;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    if (std::getenv("HC_DEBUG")) std::fprintf(stderr, "libhc: %s: %s\n", what, cudaGetErrorString(e));
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(e == cudaErrorMemoryAllocation ? HC_ENOMEM : HC_ECUDA);
+}
+
+int check_params(const uint8_t *x, size_t m, int q, int alpha) {
+    if (m == 0 || x == nullptr || q < 1) return HC_EINVAL;
+    if (m > HC_MAX_PATTERN) return HC_ETOOLONG;
+    if (static_cast<size_t>(q) > m) return HC_ETOOSHORT;
+    if (q > 8) return HC_EINVAL;
+    if (alpha < 1 || alpha > HC_MAX_ALPHA) return HC_EALPHA;
+    return HC_OK;
+}
+
+// Fig. 3 Preprocessing result for x (see the file header for the construction).
+void build_table(const uint8_t *x, uint32_t m, uint32_t q, uint32_t alpha, uint32_t *F,
+                 uint32_t *s_out, uint32_t *hv_out) {
+    const uint32_t s = alpha / q;                 // Eq. 4
+    const uint32_t mask = (1u << alpha) - 1u;     // F'
+    const uint32_t ng = m - q + 1;                // q-grams of x
+    std::vector<uint32_t> h(ng);
+    for (uint32_t i = 0; i < ng; ++i) {           // h of x[i .. i+q-1]: sum_k x[i+k] 2^(s k)
+        uint32_t v = 0;
+        for (uint32_t k = 0; k < q; ++k) v += static_cast<uint32_t>(x[i + k]) << (s * k);
+        h[i] = v & mask;
+    }
+    std::fill(F, F + (1u << alpha), 0u);
+    for (uint32_t i = 0; i + 2 * q <= m; ++i)     // Eq. 1: u1 = x[i..i+q-1], u2 = next q bytes
+        F[h[i + q]] |= 1u << (h[i] & (HC_WORD_BITS - 1));
+    const uint32_t nfirst = std::min(q, ng);      // Eq. 2 + optimisation 1
+    for (uint32_t i = 0; i < nfirst; ++i)
+        if (F[h[i]] == 0) F[h[i]] = 1;
+    *s_out = s;
+    *hv_out = h[m % q];                           // first q-gram of the chain ending at m-1
+}
+
+struct Pinned {
+    uint32_t *p = nullptr;
+};
+thread_local Pinned g_pinned;
+
+uint32_t *pinned_word() {
+    if (!g_pinned.p) {
+        void *v = nullptr;
+        if (cudaHostAlloc(&v, 64, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+        g_pinned.p = static_cast<uint32_t *>(v);
+    }
+    return g_pinned.p;
+}
+
+std::once_flag g_pool_once[64];
+void tune_pool(int dev) {
+    if (dev < 0 || dev >= 64) return;
+    std::call_once(g_pool_once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int sm_count(int dev) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 1;
+}
+
+int max_smem_optin(int dev) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v > 0 ? v : 48 * 1024;
+}
+
+// Default path choice: stage the whole text when the shift is
+// small enough that HC touches every 32-B sector anyway; gather otherwise.
+constexpr uint32_t kStagedMaxShift = 96;
+constexpr uint32_t kDefaultStageBytes = 16384;
+constexpr uint32_t kDefaultStages = 3;
+constexpr uint32_t kDefaultSegPerLane = 4;
+
+}  // namespace
+
+extern "C" {
+
+const char *hc_version(void) { return "hc-b200 0.1 (sm_100a)"; }
+
+int hc_last_error(void) { return g_last_error; }
+
+const char *hc_strerror(int code) {
+    switch (code) {
+        case HC_OK: return "ok";
+        case HC_EINVAL: return "invalid argument";
+        case HC_ETOOSHORT: return "pattern shorter than q (q > m)";
+        case HC_EALPHA: return "alpha outside [1, 15]";
+        case HC_ENOMEM: return "out of memory";
+        case HC_ECUDA: return "CUDA runtime error";
+        case HC_ETOOLONG: return "text or pattern too long";
+        case HC_ENODEV: return "no usable CUDA device";
+        default: return "unknown error";
+    }
+}
+
+int hc_build_table(const uint8_t *x, size_t m, int q, int alpha, uint32_t *F_out, int *s_out,
+                   uint32_t *hv_out) {
+    const int rc = check_params(x, m, q, alpha);
+    if (rc != HC_OK) return fail(rc);
+    if (!F_out) return fail(HC_EINVAL);
+    uint32_t s = 0, hv = 0;
+    build_table(x, static_cast<uint32_t>(m), static_cast<uint32_t>(q), static_cast<uint32_t>(alpha),
+                F_out, &s, &hv);
+    if (s_out) *s_out = static_cast<int>(s);
+    if (hv_out) *hv_out = hv;
+    return HC_OK;
+}
+
+hc_handle *hc_prepare(const uint8_t *x, size_t m, int q, int alpha) {
+    const int rc = check_params(x, m, q, alpha);
+    if (rc != HC_OK) {
+        fail(rc);
+        return nullptr;
+    }
+    hc_handle *h = new (std::nothrow) hc_handle();
+    if (!h) {
+        fail(HC_ENOMEM);
+        return nullptr;
+    }
+    h->m = static_cast<uint32_t>(m);
+    h->q = static_cast<uint32_t>(q);
+    h->alpha = static_cast<uint32_t>(alpha);
+    h->mask = (1u << alpha) - 1u;
+    h->x.assign(x, x + m);
+    h->F.assign(1u << alpha, 0u);
+    build_table(x, h->m, h->q, h->alpha, h->F.data(), &h->s, &h->hv);
+
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e != cudaSuccess) {
+        delete h;
+        cuda_fail(e, "cudaGetDevice");
+        g_last_error = HC_ENODEV;
+        return nullptr;
+    }
+    e = cudaMalloc(&h->dF, h->F.size() * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&h->dx, m + 16);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(h->dF, h->F.data(), h->F.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->dx, x, m, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "hc_prepare upload");
+        hc_destroy(h);
+        return nullptr;
+    }
+    g_last_error = HC_OK;
+    return h;
+}
+
+void hc_destroy(hc_handle *h) {
+    if (!h) return;
+    if (h->dF) cudaFree(h->dF);
+    if (h->dx) cudaFree(h->dx);
+    delete h;
+}
+
+int hc_table(const hc_handle *h, const uint32_t **F, int *alpha, int *s, int *w, uint32_t *h_v) {
+    if (!h) return fail(HC_EINVAL);
+    if (F) *F = h->F.data();
+    if (alpha) *alpha = static_cast<int>(h->alpha);
+    if (s) *s = static_cast<int>(h->s);
+    if (w) *w = HC_WORD_BITS;
+    if (h_v) *h_v = h->hv;
+    return HC_OK;
+}
+
+int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t *pos_out,
+                     size_t max_out, cudaStream_t stream, const hc_search_opts *opts,
+                     hc_search_stats *stats) {
+    if (!h) return fail(HC_EINVAL);
+    if (n > 0 && !y_dev) return fail(HC_EINVAL);
+    if (n > HC_MAX_TEXT) return fail(HC_ETOOLONG);
+    hc_search_opts o{};
+    if (opts) o = *opts;
+    if (stats) *stats = hc_search_stats{};
+    g_last_error = HC_OK;
+    if (n < h->m) return 0;  // S:123, reading R9
+
+    DeviceGuard guard(h->device);
+    tune_pool(h->device);
+    const bool want_pos = pos_out != nullptr && max_out > 0;
+    const uint32_t m = h->m, q = h->q;
+    const uint32_t S = m - q + 1;
+    const uint32_t nn = static_cast<uint32_t>(n);
+    const uint32_t windows = nn - m + 1;
+    const uint32_t K = (windows + S - 1) / S;
+
+    hc::KParams p{};
+    p.y = y_dev;
+    p.n = nn;
+    p.F = h->dF;
+    p.x = h->dx;
+    p.m = m;
+    p.q = q;
+    p.s = h->s;
+    p.mask = h->mask;
+    p.hv = h->hv;
+    p.S = S;
+    p.alpha = h->alpha;
+    p.K = K;
+
+    int path = o.path;
+    if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STAGED : HC_PATH_GATHER;
+    if (path == HC_PATH_STAGED) {
+        uint32_t stage = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultStageBytes;
+        // at least 32 segments (one per lane of a warp) per tile
+        const uint32_t need = 32 * S + m + 48;
+        if (stage < need) stage = need;
+        stage = (stage + 15) & ~15u;
+        p.stages = o.stages > 0 ? static_cast<uint32_t>(o.stages) : kDefaultStages;
+        p.stage_bytes = stage;
+        // segments whose bytes [k0*S, m-1+k1*S) fit with 16 B of misalignment slack at
+        // each end: (k1-k0)*S + m - 1 + 32 <= stage
+        p.seg_per_tile = (stage - 32 - (m - 1)) / S;
+        p.ntiles = (K + p.seg_per_tile - 1) / p.seg_per_tile;
+        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages);
+        if (smem > max_smem_optin(h->device)) {
+            if (o.path == HC_PATH_STAGED) return fail(HC_EINVAL);
+            path = HC_PATH_GATHER;
+        }
+    }
+    if (path == HC_PATH_GATHER) {
+        const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)
+                                                : kDefaultSegPerLane;
+        p.seg_per_chunk = 32 * spl;
+        p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
+        if (hc::gather_smem_bytes(p.alpha, m) > max_smem_optin(h->device)) return fail(HC_EINVAL);
+    }
+
+    // scratch: [counter | positions]
+    uint32_t cap = 0;
+    if (want_pos) {
+        const size_t want = std::max<size_t>(max_out, size_t(1) << 16);
+        cap = static_cast<uint32_t>(std::min<size_t>(want, windows));
+    }
+    uint32_t *pin = pinned_word();
+    if (!pin) return fail(HC_ENOMEM);
+
+    int launches = 0, reruns = 0;
+    uint32_t count = 0;
+    float kms = 0.f;
+    hc::LaunchInfo li;
+    for (int attempt = 0;; ++attempt) {
+        uint32_t *scratch = nullptr;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&scratch),
+                                        (static_cast<size_t>(cap) + 4) * sizeof(uint32_t), stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync scratch");
+        p.counter = scratch;
+        p.out = want_pos ? scratch + 4 : nullptr;
+        p.cap = cap;
+        e = cudaMemsetAsync(scratch, 0, sizeof(uint32_t), stream);
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        const bool timed = o.time_kernel && attempt == 0;
+        if (timed) {
+            cudaEventCreate(&ev0);
+            cudaEventCreate(&ev1);
+            cudaEventRecord(ev0, stream);
+        }
+        if (e == cudaSuccess)
+            e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, &li)
+                                       : hc::launch_gather(p, stream, o.max_ctas, &li);
+        ++launches;
+        if (timed) cudaEventRecord(ev1, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(pin, scratch, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (timed) {
+            if (e == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
+            cudaEventDestroy(ev0);
+            cudaEventDestroy(ev1);
+        }
+        if (e != cudaSuccess) {
+            cudaFreeAsync(scratch, stream);
+            return cuda_fail(e, "search kernel");
+        }
+        count = *pin;
+        if (want_pos && count > cap) {
+            // position scratch overflowed: the count is exact, re-run with room for all
+            cudaFreeAsync(scratch, stream);
+            cap = count;
+            ++reruns;
+            continue;
+        }
+        if (want_pos && count > 0) {
+            const uint32_t k = static_cast<uint32_t>(std::min<size_t>(count, max_out));
+            e = hc::sort_and_widen(scratch + 4, count, nn, pos_out, k, stream, &launches);
+        }
+        cudaError_t e2 = cudaFreeAsync(scratch, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "sort");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
+        break;
+    }
+    if (stats) {
+        stats->path = path;
+        stats->grid = li.grid;
+        stats->block = li.block;
+        stats->smem_bytes = li.smem;
+        stats->tiles = path == HC_PATH_STAGED ? p.ntiles : p.nchunks;
+        stats->launches = launches;
+        stats->reruns = reruns;
+        stats->kernel_ms = kms;
+    }
+    return static_cast<int64_t>(count);
+}
+
+int64_t hc_search(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t *pos_out,
+                  size_t max_out, cudaStream_t stream) {
+    return hc_search_ex(h, y_dev, n, pos_out, max_out, stream, nullptr, nullptr);
+}
+
+int64_t hc_search_host(const hc_handle *h, const uint8_t *y_host, size_t n, int64_t *pos_out_host,
+                       size_t max_out, cudaStream_t stream) {
+    if (!h) return fail(HC_EINVAL);
+    if (n > 0 && !y_host) return fail(HC_EINVAL);
+    if (n > HC_MAX_TEXT) return fail(HC_ETOOLONG);
+    g_last_error = HC_OK;
+    if (n < h->m) return 0;
+    DeviceGuard guard(h->device);
+    tune_pool(h->device);
+    const bool want_pos = pos_out_host != nullptr && max_out > 0;
+    const size_t k_cap = want_pos ? std::min<size_t>(max_out, n - h->m + 1) : 0;
+    uint8_t *dy = nullptr;
+    int64_t *dpos = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&dy), n, stream);
+    if (e == cudaSuccess && want_pos) e = cudaMallocAsync(reinterpret_cast<void **>(&dpos), k_cap * 8, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dy, y_host, n, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) {
+        if (dy) cudaFreeAsync(dy, stream);
+        if (dpos) cudaFreeAsync(dpos, stream);
+        return cuda_fail(e, "hc_search_host upload");
+    }
+    const int64_t cnt = hc_search_ex(h, dy, n, dpos, k_cap, stream, nullptr, nullptr);
+    if (cnt > 0 && want_pos) {
+        const size_t k = std::min<size_t>(static_cast<size_t>(cnt), k_cap);
+        e = cudaMemcpyAsync(pos_out_host, dpos, k * 8, cudaMemcpyDeviceToHost, stream);
+    }
+    cudaFreeAsync(dy, stream);
+    if (dpos) cudaFreeAsync(dpos, stream);
+    cudaError_t e2 = cudaStreamSynchronize(stream);
+    if (cnt < 0) return cnt;
+    if (e != cudaSuccess) return cuda_fail(e, "hc_search_host read-back");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "hc_search_host sync");
+    return cnt;
+}
+
+}  // extern "C"

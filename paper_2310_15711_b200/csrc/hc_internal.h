@@ -1,0 +1,54 @@
+// Internal interface between the host side (hc_api.cpp) and the device side
+// (hc_kernels.cu) of libhc.  Not part of the C-ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hc {
+
+// Everything one search kernel launch needs (passed by value).
+struct KParams {
+    const uint8_t *y;    // text, device, any alignment
+    uint32_t n;          // text length (n >= m, n <= HC_MAX_TEXT)
+    const uint32_t *F;   // filter table, device, 2^alpha words
+    const uint8_t *x;    // pattern, device
+    uint32_t m, q, s, mask, hv;
+    uint32_t S;          // shift m - q + 1: also the segment length
+    uint32_t alpha;
+    uint32_t K;          // number of segments: ceil((n - m + 1) / S)
+    // staged path
+    uint32_t seg_per_tile;  // segments per shared-memory tile
+    uint32_t ntiles;
+    uint32_t stage_bytes;   // bytes per stage buffer (multiple of 16)
+    uint32_t stages;
+    // gather path
+    uint32_t seg_per_chunk; // segments per warp chunk
+    uint32_t nchunks;
+    // output
+    uint32_t *out;       // positions (window starts), unordered; NULL = count only
+    uint32_t cap;        // capacity of out
+    uint32_t *counter;   // [0] = total occurrences (may exceed cap)
+};
+
+struct LaunchInfo {
+    int grid = 0, block = 0, smem = 0;
+};
+
+// Device-side entry points (hc_kernels.cu).  All enqueue on `st`.
+cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li);
+cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li);
+// Sort positions[0..count) ascending and write the first `k` as int64 into dst.
+// `count` and `k` are host values.  May allocate temporaries (stream-ordered).
+cudaError_t sort_and_widen(uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
+                           uint32_t k, cudaStream_t st, int *launches);
+
+int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages);
+int gather_smem_bytes(uint32_t alpha, uint32_t m);
+
+constexpr int kStagedThreads = 256;
+constexpr int kGatherThreads = 256;
+constexpr int kWarpBuf = 64;  // per-warp match buffer entries (shared memory)
+
+}  // namespace hc

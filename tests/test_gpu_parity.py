@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by
+element, on seeded inputs sized so the oracle finishes in seconds but the
+kernels see many tiles, many lane chunks and ragged tails.  Bit-exact: same
+count, same ascending position list (integer work)."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2310_15711_b200 import hc  # noqa: E402
+from paper_2310_15711_b200 import inputs as I  # noqa: E402
+
+PATHS = [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_AUTO]
+
+
+def to_dev(y: np.ndarray, offset: int = 0):
+    """y on the device starting `offset` bytes past a 256-aligned allocation."""
+    buf = torch.empty(len(y) + offset + 1, dtype=torch.uint8, device="cuda")
+    buf[len(y) + offset:] = 0xA5
+    if len(y):
+        buf[offset:offset + len(y)] = torch.from_numpy(np.ascontiguousarray(y)).cuda()
+    return buf[offset:offset + len(y)]
+
+
+def gpu(h, y_dev, max_out=None, **kw):
+    res = hc.search(h, y_dev, max_out=max_out, **kw)
+    torch.cuda.synchronize()
+    return res.cpu().numpy()
+
+
+def test_table_parity_with_oracle():
+    rng = np.random.default_rng(51)
+    for _ in range(100):
+        q = int(rng.integers(1, 9))
+        m = int(rng.integers(q, 200))
+        alpha = int(rng.integers(1, 16))
+        x = rng.integers(0, 256, m, dtype=np.uint8)
+        h = hc.prepare(x, q, alpha)
+        t = h.table()
+        o = oracle.preprocess(x, q, alpha, w=32)
+        assert np.array_equal(t.F.astype(np.uint64), o.F) and t.hv == o.hv and t.s == o.s
+
+
+def test_spec_examples():
+    y = to_dev(np.frombuffer(b"aaaa", np.uint8))
+    for q in (1, 2):
+        for path in PATHS:
+            assert gpu(hc.prepare(b"aa", q, 8), y, path=path).tolist() == [0, 1, 2]
+    y = to_dev(np.frombuffer(b"zzzz", np.uint8))
+    assert gpu(hc.prepare(b"abc", 2, 8), y).tolist() == []
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_random_small(path):
+    rng = np.random.default_rng(52 + path)
+    for trial in range(120):
+        sigma = int(rng.choice([2, 4, 20, 64, 256]))
+        q = int(rng.integers(1, 9))
+        m = int(rng.integers(q, 140))
+        alpha = int(rng.integers(8, 13))
+        n = int(rng.integers(0, 60_000))
+        y = rng.integers(0, sigma, n, dtype=np.uint8)
+        if n >= m and rng.random() < 0.8:
+            o = int(rng.integers(0, n - m + 1))
+            x = y[o:o + m].copy()
+            for p in rng.integers(0, n - m + 1, 5):
+                y[p:p + m] = x
+        else:
+            x = rng.integers(0, sigma, m, dtype=np.uint8)
+        want = oracle.brute(x, y)
+        h = hc.prepare(x, q, alpha)
+        off = int(rng.integers(0, 16))
+        got = gpu(h, to_dev(y, off), path=path)
+        assert np.array_equal(got, want), (trial, m, q, alpha, n, off, len(want), len(got))
+
+
+@pytest.mark.parametrize("path", [hc.PATH_STAGED, hc.PATH_GATHER])
+@pytest.mark.parametrize("max_ctas,stages", [(1, 2), (2, 3), (3, 4), (5, 1)])
+def test_many_tiles_per_cta(path, max_ctas, stages):
+    # tiny tiles / few CTAs: every CTA cycles its TMA ring many times
+    rng = np.random.default_rng(53)
+    y = I.gen_text("dna", 300_001, 53)
+    for m, q in [(8, 4), (16, 6), (32, 6), (33, 3), (100, 8), (7, 7)]:
+        x = y[12345:12345 + m].copy()
+        yy = y.copy()
+        for p in rng.integers(0, len(y) - m, 40):
+            yy[p:p + m] = x
+        want = oracle.brute(x, yy)
+        h = hc.prepare(x, q, 12)
+        got = gpu(h, to_dev(yy, 3), path=path, tile_bytes=64, stages=stages, max_ctas=max_ctas,
+                  seg_per_lane=1)
+        assert np.array_equal(got, want), (m, q)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_plant_at_every_offset_near_tile_and_text_edges(path):
+    # occurrences at every offset within +-m of text ends; texts of every length
+    # around m and ragged tails
+    rng = np.random.default_rng(54)
+    for m, q in [(5, 2), (16, 6), (40, 4)]:
+        x = rng.integers(200, 256, m, dtype=np.uint8)  # bytes >= 0x80
+        for n in list(range(0, m + 3)) + [m + 31, 2 * m + 17, 1000, 4099]:
+            base = rng.integers(0, 4, n, dtype=np.uint8)
+            ps = [p for p in range(0, max(0, n - m + 1)) if p < m + 2 or p > n - 2 * m - 2]
+            for p in ps[:: max(1, len(ps) // 12)] if ps else [None]:
+                y = base.copy()
+                if p is not None:
+                    y[p:p + m] = x
+                want = oracle.brute(x, y)
+                for off in (0, 7, 15):
+                    got = gpu(hc.prepare(x, q, 11), to_dev(y, off), path=path)
+                    assert np.array_equal(got, want), (m, n, p, off)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_all_positions_match(path):
+    # a^m in a^n: n-m+1 occurrences: every window completes its walk and verifies
+    for m, q, n in [(1, 1, 5000), (2, 2, 70_000), (8, 3, 40_000), (64, 6, 100_000), (300, 8, 50_000)]:
+        h = hc.prepare(b"a" * m, q, 12)
+        got = gpu(h, to_dev(np.full(n, ord("a"), np.uint8), 5), path=path)
+        assert len(got) == n - m + 1
+        assert np.array_equal(got, np.arange(n - m + 1))
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_max_out_and_count_only(path):
+    rng = np.random.default_rng(55)
+    y = rng.integers(0, 2, 200_000, dtype=np.uint8)
+    x = y[500:510].copy()
+    want = oracle.brute(x, y)
+    assert len(want) > 100
+    h = hc.prepare(x, 5, 10)
+    yd = to_dev(y)
+    assert hc.count(h, yd, path=path) == len(want)
+    for k in (1, 7, len(want) - 1, len(want), len(want) + 10):
+        got = gpu(h, yd, max_out=k, path=path)
+        assert np.array_equal(got, want[:k])
+
+
+def test_scratch_overflow_rerun():
+    # more occurrences than the default scratch (2^16): the library re-runs with room
+    n = 300_000
+    y = np.zeros(n, np.uint8)
+    h = hc.prepare(bytes(3), 3, 12)
+    res, st = hc.search(h, to_dev(y), max_out=10, stats=True)
+    assert st["reruns"] == 1
+    assert res.cpu().numpy().tolist() == list(range(10))
+    assert hc.count(h, to_dev(y)) == n - 2
+
+
+def test_host_entry_point():
+    rng = np.random.default_rng(56)
+    y = rng.integers(0, 4, 123_457, dtype=np.uint8)
+    x = y[999:1031].copy()
+    h = hc.prepare(x, 6, 12)
+    assert np.array_equal(hc.search_host(h, y), oracle.brute(x, y))
+    assert hc.search_host(h, y[:10]).tolist() == []
+
+
+def test_errors():
+    h = hc.prepare(b"abcd", 2, 8)
+    with pytest.raises(hc.HCError) as ei:
+        hc.search_raw(h, 0, 100, None, 0, 0)
+    assert ei.value.code == hc.HC_EINVAL
+    assert hc.search_raw(h, 0, 0, None, 0, 0) == 0          # n = 0 -> 0
+    with pytest.raises(hc.HCError):
+        hc.prepare(b"ab", 3, 8)
+
+
+def test_c1_config_exact():
+    cfg = I.CONFIGS["C1"]
+    y, _ = I.config_text(cfg)
+    yd = to_dev(y)
+    q, a = cfg.qa[32]
+    for o, x in I.patterns(cfg, y, 32):
+        want = oracle.brute(x, y)
+        assert o in want.tolist()
+        for path in PATHS:
+            assert np.array_equal(gpu(hc.prepare(x, q, a), yd, path=path), want)
