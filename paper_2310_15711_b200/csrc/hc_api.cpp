@@ -43,7 +43,7 @@ int fail(int code) {
 }
 
 int cuda_fail(cudaError_t e, const char *what) {
-    if (std::getenv("HC_DEBUG")) std::fprintf(stderr, "libhc: %s: %s\n", what, cudaGetErrorString(e));
+    if (std::getenv("HC_DEBUG")) std::fprintf(stderr, "libhc: %s: %s (%s)\n", what, cudaGetErrorString(e), cudaGetErrorName(e));
     cudaGetLastError();  // clear sticky-free errors
     return fail(e == cudaErrorMemoryAllocation ? HC_ENOMEM : HC_ECUDA);
 }
@@ -79,18 +79,49 @@ void build_table(const uint8_t *x, uint32_t m, uint32_t q, uint32_t alpha, uint3
     *hv_out = h[m % q];                           // first q-gram of the chain ending at m-1
 }
 
-struct Pinned {
-    uint32_t *p = nullptr;
+// Per-host-thread, per-device scratch: [counter (16 B) | positions (cap u32)] plus a
+// mapped pinned word the finish kernel writes the count into.  hc_search returns only
+// after all of its device work completed, so the next call on this thread (any
+// stream) can reuse it; the counter is zeroed once here and reset by every finish
+// kernel afterwards.
+struct Scratch {
+    int dev = -1;
+    uint32_t *buf = nullptr;       // device
+    size_t cap = 0;                // position capacity
+    uint32_t *host_count = nullptr;      // pinned, mapped
+    uint32_t *host_count_dev = nullptr;  // its device alias
 };
-thread_local Pinned g_pinned;
+thread_local Scratch g_scratch[8];
 
-uint32_t *pinned_word() {
-    if (!g_pinned.p) {
-        void *v = nullptr;
-        if (cudaHostAlloc(&v, 64, cudaHostAllocDefault) != cudaSuccess) return nullptr;
-        g_pinned.p = static_cast<uint32_t *>(v);
+cudaError_t get_scratch(int dev, size_t cap, Scratch **out) {
+    if (dev < 0 || dev >= 8) return cudaErrorInvalidDevice;
+    Scratch &sc = g_scratch[dev];
+    if (!sc.host_count) {
+        void *hp = nullptr;
+        cudaError_t e = cudaHostAlloc(&hp, 64, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return e;
+        void *dp = nullptr;
+        e = cudaHostGetDevicePointer(&dp, hp, 0);
+        if (e != cudaSuccess) return e;
+        sc.host_count = static_cast<uint32_t *>(hp);
+        sc.host_count_dev = static_cast<uint32_t *>(dp);
     }
-    return g_pinned.p;
+    if (!sc.buf || sc.cap < cap) {
+        if (sc.buf) cudaFree(sc.buf);
+        sc.buf = nullptr;
+        const size_t want = std::max<size_t>(cap, sc.cap + sc.cap / 2);
+        cudaError_t e = cudaMalloc(&sc.buf, 16 + want * sizeof(uint32_t));
+        if (e != cudaSuccess) {
+            sc.cap = 0;
+            return e;
+        }
+        e = cudaMemset(sc.buf, 0, 16);
+        if (e != cudaSuccess) return e;
+        sc.cap = want;
+    }
+    sc.dev = dev;
+    *out = &sc;
+    return cudaSuccess;
 }
 
 std::once_flag g_pool_once[64];
@@ -291,27 +322,21 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     }
 
     // scratch: [counter | positions]
-    uint32_t cap = 0;
-    if (want_pos) {
-        const size_t want = std::max<size_t>(max_out, size_t(1) << 16);
-        cap = static_cast<uint32_t>(std::min<size_t>(want, windows));
-    }
-    uint32_t *pin = pinned_word();
-    if (!pin) return fail(HC_ENOMEM);
+    size_t cap = 0;
+    if (want_pos) cap = std::min<size_t>(std::max<size_t>(max_out, size_t(1) << 16), windows);
+    const uint32_t k_out = want_pos ? static_cast<uint32_t>(std::min<size_t>(max_out, windows)) : 0;
 
     int launches = 0, reruns = 0;
     uint32_t count = 0;
     float kms = 0.f;
     hc::LaunchInfo li;
     for (int attempt = 0;; ++attempt) {
-        uint32_t *scratch = nullptr;
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&scratch),
-                                        (static_cast<size_t>(cap) + 4) * sizeof(uint32_t), stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync scratch");
-        p.counter = scratch;
-        p.out = want_pos ? scratch + 4 : nullptr;
-        p.cap = cap;
-        e = cudaMemsetAsync(scratch, 0, sizeof(uint32_t), stream);
+        Scratch *sc = nullptr;
+        cudaError_t e = get_scratch(h->device, cap, &sc);
+        if (e != cudaSuccess) return cuda_fail(e, "scratch");
+        p.counter = sc->buf;
+        p.out = want_pos ? sc->buf + 4 : nullptr;
+        p.cap = static_cast<uint32_t>(cap);
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         const bool timed = o.time_kernel && attempt == 0;
         if (timed) {
@@ -319,37 +344,46 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             cudaEventCreate(&ev1);
             cudaEventRecord(ev0, stream);
         }
-        if (e == cudaSuccess)
-            e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, &li)
-                                       : hc::launch_gather(p, stream, o.max_ctas, &li);
+        const char *stage = "search kernel launch";
+        e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, &li)
+                                   : hc::launch_gather(p, stream, o.max_ctas, &li);
         ++launches;
         if (timed) cudaEventRecord(ev1, stream);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(pin, scratch, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e == cudaSuccess) {
+            stage = "finish kernel launch";
+            *sc->host_count = 0xffffffffu;
+            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, sc->host_count_dev, stream);
+            ++launches;
+        }
+        if (e == cudaSuccess) {
+            stage = "search/finish execution";
+            e = cudaStreamSynchronize(stream);
+        }
         if (timed) {
             if (e == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
             cudaEventDestroy(ev0);
             cudaEventDestroy(ev1);
         }
         if (e != cudaSuccess) {
-            cudaFreeAsync(scratch, stream);
-            return cuda_fail(e, "search kernel");
+            // the counter may be left non-zero: force a fresh scratch next time
+            cudaFree(sc->buf);
+            sc->buf = nullptr;
+            sc->cap = 0;
+            return cuda_fail(e, stage);
         }
-        count = *pin;
+        count = *reinterpret_cast<volatile uint32_t *>(sc->host_count);
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all
-            cudaFreeAsync(scratch, stream);
             cap = count;
             ++reruns;
             continue;
         }
-        if (want_pos && count > 0) {
+        if (want_pos && count > hc::kSmallSort) {
             const uint32_t k = static_cast<uint32_t>(std::min<size_t>(count, max_out));
-            e = hc::sort_and_widen(scratch + 4, count, nn, pos_out, k, stream, &launches);
+            e = hc::sort_large(sc->buf + 4, count, nn, pos_out, k, stream, &launches);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+            if (e != cudaSuccess) return cuda_fail(e, "sort");
         }
-        cudaError_t e2 = cudaFreeAsync(scratch, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "sort");
-        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync");
         break;
     }
     if (stats) {

@@ -39,10 +39,14 @@ struct LaunchInfo {
 // Device-side entry points (hc_kernels.cu).  All enqueue on `st`.
 cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li);
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li);
-// Sort positions[0..count) ascending and write the first `k` as int64 into dst.
-// `count` and `k` are host values.  May allocate temporaries (stream-ordered).
-cudaError_t sort_and_widen(uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
-                           uint32_t k, cudaStream_t st, int *launches);
+// One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,
+// ordering of <= kSmallSort positions into dst (first min(count, max_out), int64).
+cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
+                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st);
+// Ordering of count > kSmallSort positions (CUB radix sort), first k written as int64.
+cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
+                       uint32_t k, cudaStream_t st, int *launches);
+constexpr uint32_t kSmallSort = 8192;
 
 int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages);
 int gather_smem_bytes(uint32_t alpha, uint32_t m);

@@ -2,37 +2,50 @@
 // (Fig. 5 left) as data-parallel CUDA kernels.
 //
 // Data parallelism (reading R11): the window ends
-// [m-1, n) are cut into K segments of S = m-q+1 ends, a_k = m-1 + k*S.  HC
-// started at a_k with loop bound b = min(a_k + S, n) reports exactly the
-// occurrences ending in [a_k, b) and reads only y[a_k-m+1 .. b-1].  A segment
-// whose first window is rejected by the F[v] == 0 fast path is done
-// after one hash; the others continue the paper's loop inside the segment.
+// [m-1, n) are cut into K segments of S = m-q+1 ends, a_k = m-1 + k*S (the
+// "lattice").  HC started at a_k with loop bound b = min(a_k + S, n) reports
+// exactly the occurrences ending in [a_k, b) and reads only y[a_k-m+1 .. b-1].
 //
-// Each lane runs the loop of Fig. 5 as a flat state machine doing ONE q-gram
-// hash per iteration (window-end hash, l.4-6, or one walk step, l.9-13), so the
-// 32 lanes of a warp stay converged; a lane whose segment is finished takes
-// the next segment of the warp's range in the same iteration (ballot/popc).
-//
-// Two text access paths (DESIGN.md 5):
+// Two phases per warp:
+//   A. filter:   every lane hashes the q-gram ending at one lattice point a_k
+//                (Fig. 5 l.4-5) and tests F[v] != 0 (l.6).  F[v] == 0 means the
+//                segment is finished (the l.18 shift lands on a_{k+1});
+//                on the paper's workloads 66-99% of segments end here.  The
+//                survivors are compacted into a per-warp queue (ballot/popc).
+//   B. survivor: 32 queued segments at a time, one per lane, continue the
+//                paper's loop inside their segment as a flat state machine that
+//                does ONE q-gram hash per iteration (window-end hash l.4-6 or
+//                one walk step l.9-13), keeping the warp converged.  Long walks
+//                (>= kLongWalk remaining steps) are done by the whole warp, 32
+//                steps at a time (same link tests, same break point), and long
+//                verifications (m > kCoopVerifyMin) compare 256 bytes per warp
+//                step.
+// Two text access paths:
 //   staged : persistent CTAs stream tiles of the text into shared memory with
-//            TMA bulk copies (cp.async.bulk + mbarrier), NSTAGE-deep ring; every
-//            hash reads shared memory.  For small shifts (every 32-B sector of
-//            the text is touched anyway).
-//   gather : no staging; each lane reads only the aligned 8-byte words holding
-//            the q-grams it hashes (ld.global.nc).  For large shifts, where HC
+//            TMA bulk copies (cp.async.bulk + mbarrier ring); every hash reads
+//            shared memory.  For small shifts, where every 32-B sector of the
+//            text is touched anyway.
+//   gather : no staging; lanes read only the aligned 8-byte words holding the
+//            q-grams they hash (ld.global.nc).  For large shifts, where HC
 //            touches a small fraction of the text (sublinear search).
 // F (2^alpha u32 words) and x live in shared memory in both paths.
-// Matches go to a per-warp shared buffer and are flushed 32 at a time with one
-// atomicAdd per flush (ballot/popc ranks); the host sorts them afterwards.
+// Matches go to a per-warp shared buffer, flushed 32 at a time with one
+// atomicAdd (ballot/popc ranks); the host orders them afterwards.
 
 #include <cub/device/device_radix_sort.cuh>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "hc_internal.h"
 
 namespace hc {
 
 #define HC_FULL 0xffffffffu
-constexpr uint32_t kWordBits = 32;  // w (R2)
+constexpr uint32_t kWordBits = 32;       // w (R2)
+constexpr uint32_t kLongWalk = 12;       // walks with >= this many steps left go warp-wide
+constexpr uint32_t kCoopVerifyMin = 64;  // m above which verification is warp-wide
+constexpr int kUnroll = 4;               // lattice rounds whose loads are issued together
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -80,6 +93,17 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
     return r;
 }
+// 64-bit shifts with PTX semantics: amounts >= 64 give 0 (clamped), no select needed.
+__device__ __forceinline__ uint64_t shr64(uint64_t a, uint32_t s) {
+    uint64_t r;
+    asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(a), "r"(s));
+    return r;
+}
+__device__ __forceinline__ uint64_t shl64(uint64_t a, uint32_t s) {
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(a), "r"(s));
+    return r;
+}
 
 // ------------------------------------------------------------------ text access
 // Text byte p (0 <= p < n) of y, read from global memory (read-only path).
@@ -109,7 +133,7 @@ struct SmemText {
 };
 
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
-// top Q bytes are meaningful: reads just the aligned 8-byte words holding y[p]
+// top Q bytes are meaningful.  Reads just the aligned 8-byte words holding y[p]
 // and y[p-Q+1] (both inside the text), so no byte outside [0, n) is touched.
 template <int Q, class T>
 __device__ __forceinline__ uint64_t end8(const T &t, uint32_t p) {
@@ -119,29 +143,59 @@ __device__ __forceinline__ uint64_t end8(const T &t, uint32_t p) {
     const uint32_t off = static_cast<uint32_t>(a & 7);
     const uint64_t hi = t.word(ah);
     uint64_t lo = 0;
-    if (Q > 1) {
-        if (T::kLoSafe || off < static_cast<uint32_t>(Q - 1)) lo = t.word(ah - 8);
+    if constexpr (Q > 1) {
+        if (T::kLoSafe || off + 1 < static_cast<uint32_t>(Q)) lo = t.word(ah - 8);
     }
-    return off == 7 ? hi : ((lo >> (8 * (off + 1))) | (hi << (56 - 8 * off)));
+    return shr64(lo, 8 * (off + 1)) | shl64(hi, 56 - 8 * off);
 }
 
 // Eq. 3 / Fig. 3 Hash: v = 0; for i = p downto p-q+1:
-// v = (v << s) + y[i]; return v & mask.  W holds y[p-7..p], byte 7 = y[p].
-template <int Q>
-__device__ __forceinline__ uint32_t qhash(uint64_t W, uint32_t s, uint32_t mask) {
-    const uint32_t whi = static_cast<uint32_t>(W >> 32), wlo = static_cast<uint32_t>(W);
+// v = (v << s) + y[i]; return v & mask, i.e. v = sum_i c_i 2^(s i) with c_0 the
+// first byte of the q-gram (reading R4).  With q and s compile-time, the sum is
+// evaluated with dp4a: bytes of one 32-bit half whose weights 2^(s (i - i0)) fit
+// in 8 bits form one group; v = sum_g dp4a(half_g, weights_g) << (s i0_g).
+struct HashPlan {
+    int n;
+    int reg[8];
+    uint32_t w[8];
+    int sh[8];
+};
+template <int Q, int SH>
+__host__ __device__ constexpr HashPlan make_plan() {
+    HashPlan P{0, {0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 0, 0}};
+    int i = 0;
+    while (i < Q) {
+        const int b = 8 - Q + i;  // byte of W holding c_i
+        const int reg = b >= 4 ? 1 : 0;
+        const int i0 = i;
+        uint32_t w = 0;
+        int j = i;
+        while (j < Q) {
+            const int bj = 8 - Q + j;
+            if ((bj >= 4 ? 1 : 0) != reg || SH * (j - i0) > 7) break;
+            w |= (1u << (SH * (j - i0))) << (8 * (bj & 3));
+            ++j;
+        }
+        P.reg[P.n] = reg;
+        P.w[P.n] = w;
+        P.sh[P.n] = SH * i0;
+        P.n++;
+        i = j;
+    }
+    return P;
+}
+template <int Q, int SH>
+__device__ __forceinline__ uint32_t qhash(uint64_t W, uint32_t mask) {
+    constexpr HashPlan P = make_plan<Q, SH>();
+    const uint32_t lo = static_cast<uint32_t>(W), hi = static_cast<uint32_t>(W >> 32);
     uint32_t v = 0;
 #pragma unroll
-    for (int t = 0; t < Q; ++t) {
-        const int b = 7 - t;
-        const uint32_t c = b >= 4 ? (whi >> (8 * (b - 4))) & 0xffu : (wlo >> (8 * b)) & 0xffu;
-        v = (v << s) + c;
-    }
+    for (int g = 0; g < P.n; ++g) v += __dp4a(P.reg[g] ? hi : lo, P.w[g], 0u) << P.sh[g];
     return v & mask;
 }
 
-// Fig. 5 l.16 verification: y[start .. start+m-1] == x (sx: x in shared memory,
-// 16-aligned).  8 bytes per step, then a byte tail.
+// Fig. 5 l.16 verification by one lane: y[start .. start+m-1] == x (sx: x in
+// shared memory, 16-aligned).  8 bytes per step, then a byte tail.
 template <class T>
 __device__ __noinline__ bool verify(const T &t, const uint8_t *sx, uint32_t start, uint32_t m) {
     uint32_t k = 0;
@@ -155,8 +209,64 @@ __device__ __noinline__ bool verify(const T &t, const uint8_t *sx, uint32_t star
     return true;
 }
 
+// The same comparison done by the whole warp, 8 bytes per lane per step.
+template <class T>
+__device__ __forceinline__ bool verify_warp(const T &t, const uint8_t *sx, uint32_t start,
+                                            uint32_t m, uint32_t lane) {
+    for (uint32_t k0 = 0; k0 < m; k0 += 256) {
+        const uint32_t k = k0 + 8 * lane;
+        bool bad = false;
+        if (k + 8 <= m) {
+            bad = end8<8>(t, start + k + 7) != *reinterpret_cast<const uint64_t *>(sx + k);
+        } else {
+            for (uint32_t kk = k; kk < m; ++kk) bad |= t.byte(start + kk) != sx[kk];
+        }
+        if (__any_sync(HC_FULL, bad)) return false;
+    }
+    return true;
+}
+
+// Fig. 5 l.8-13 for one lane's walk, done by the whole warp: lane t evaluates step t
+// of the next 32 (hash of the q-gram ending at j-(t+1)q, its word F[v_t]); the link
+// test of step t uses the word of step t-1 (shuffled up).  The first failing step is
+// the sequential loop's break (l.12).  On return j is the position of the last
+// evaluated step (the failing one if broke) and v its hash.
+template <int Q, int SH, class T>
+__device__ __forceinline__ void walk_warp(const KParams &p, const T &txt, const uint32_t *sF,
+                                          uint32_t lane, uint32_t &j, uint32_t i, uint32_t z,
+                                          uint32_t &v, bool &broke) {
+    uint32_t R = (j - i) / p.q + 1;  // steps while j >= i
+    broke = false;
+    while (true) {
+        const uint32_t steps = min(R, 32u);
+        const bool valid = lane < steps;
+        uint32_t vt = 0, zt = 0;
+        if (valid) {
+            vt = qhash<Q, SH>(end8<Q>(txt, j - (lane + 1) * p.q), p.mask);
+            zt = sF[vt];
+        }
+        uint32_t zprev = __shfl_up_sync(HC_FULL, zt, 1);
+        if (lane == 0) zprev = z;
+        const bool ok = (zprev >> (vt & (kWordBits - 1))) & 1u;
+        const uint32_t fm = __ballot_sync(HC_FULL, valid && !ok);
+        if (fm) {
+            const uint32_t t = __ffs(fm) - 1;
+            j -= (t + 1) * p.q;
+            v = __shfl_sync(HC_FULL, vt, t);
+            broke = true;
+            return;
+        }
+        j -= steps * p.q;
+        z = __shfl_sync(HC_FULL, zt, steps - 1);
+        v = __shfl_sync(HC_FULL, vt, steps - 1);
+        R -= steps;
+        if (R == 0) return;
+    }
+}
+
 // Per-warp match buffer: positions are appended (ballot rank) and flushed to
-// global memory 32 at a time with one atomicAdd.
+// global memory 32 at a time with one atomicAdd.  Count-only calls have cap 0:
+// the same counting, no position writes.
 struct WarpOut {
     uint32_t *buf;   // shared, kWarpBuf entries
     uint32_t cnt;    // warp-uniform
@@ -193,78 +303,152 @@ struct WarpOut {
     }
 };
 
-// Runs HC on segments [seg_lo, seg_hi) with the 32 lanes of the calling warp.
-// Every lane of the warp must call it (warp-synchronous).
-template <int Q, bool COUNT_ONLY, class T>
-__device__ __forceinline__ void run_segments(const KParams &p, const T &txt, const uint32_t *sF,
-                                             const uint8_t *sx, uint32_t seg_lo, uint32_t seg_hi,
-                                             WarpOut &wo, uint32_t &nfound, uint32_t lane) {
-    const uint32_t lt = lanemask_lt();
-    uint32_t cursor = seg_lo;
-    bool active = false, walk = false;
-    uint32_t j = 0, e = 0, i = 0, b = 0, z = 0;
-    while (true) {
-        const uint32_t idle = __ballot_sync(HC_FULL, !active);
-        if (idle != 0 && cursor < seg_hi) {
-            const uint32_t k = cursor + __popc(idle & lt);
-            if (!active && k < seg_hi) {
-                active = true;
+// Phase B: HC (Fig. 5) on `cnt` <= 32 queued segments, one per lane.  Warp-synchronous.
+template <int Q, int SH, class T>
+__device__ __noinline__ void run_survivors(const KParams &p, const T &txt, const uint32_t *sF,
+                                           const uint8_t *sx, const uint32_t *queue,
+                                           uint32_t cnt, WarpOut &wo, uint32_t lane) {
+    bool active = lane < cnt;
+    const uint32_t k = active ? queue[lane] : 0u;
+    __syncwarp();
+    uint32_t j = p.m - 1 + k * p.S;            // lattice window end a_k
+    const uint32_t b = min(j + p.S, p.n);      // segment bound
+    uint32_t e = 0, i = 0, z = 0, v = 0;
+    bool walk = false;
+    while (__any_sync(HC_FULL, active)) {
+        bool need_v = false, stepped = false;
+        // long walks: warp-wide, one lane at a time
+        uint32_t lm = __ballot_sync(HC_FULL, active && walk && (j - i) >= kLongWalk * p.q);
+        while (lm) {
+            const uint32_t L = __ffs(lm) - 1;
+            lm &= lm - 1;
+            uint32_t jL = __shfl_sync(HC_FULL, j, L);
+            const uint32_t iL = __shfl_sync(HC_FULL, i, L);
+            const uint32_t zL = __shfl_sync(HC_FULL, z, L);
+            uint32_t vL = 0;
+            bool broke = false;
+            walk_warp<Q, SH>(p, txt, sF, lane, jL, iL, zL, vL, broke);
+            if (lane == L) {
+                stepped = true;
                 walk = false;
-                j = p.m - 1 + k * p.S;                 // lattice window end a_k
-                b = min(j + p.S, p.n);                 // segment bound
-            }
-            cursor += __popc(idle);
-        }
-        if (__ballot_sync(HC_FULL, active) == 0) break;
-        bool found = false;
-        uint32_t fpos = 0;
-        if (active) {
-            const uint32_t pos = walk ? j - p.q : j;
-            const uint32_t v = qhash<Q>(end8<Q>(txt, pos), p.s, p.mask);
-            bool complete = false;
-            if (!walk) {                               // Fig. 5 l.4-7
-                e = j;
-                z = sF[v];
-                if (z == 0) {
-                    j += p.S;                          // l.18 fast path
+                v = vL;
+                if (broke) {
+                    j = jL + p.S;                              // l.12 -> l.18
                 } else {
-                    i = j + 2 * p.q - p.m;             // l.7: i = j - m + 2q (> 0)
-                    if (j >= i) walk = true;           // l.8
-                    else complete = true;              // m < 2q: while-else (R7)
+                    need_v = v == p.hv;                        // l.14-16
+                    j = e + 1;                                 // (i - q) + (m - q + 1)
                 }
-            } else {                                   // l.9-13
-                j -= p.q;
-                if (((z >> (v & (kWordBits - 1))) & 1u) == 0) {
-                    walk = false;                      // l.12 break
-                    j += p.S;                          // l.18
+                if (j >= b) active = false;
+            }
+        }
+        if (active && !stepped) {
+            const uint32_t pos = walk ? j - p.q : j;
+            const uint32_t vv = qhash<Q, SH>(end8<Q>(txt, pos), p.mask);
+            bool complete = false;
+            if (!walk) {                                       // l.4-7
+                e = j;
+                v = vv;
+                z = sF[vv];
+                if (z == 0) {
+                    j += p.S;                                  // l.18 fast path
                 } else {
-                    z = sF[v];                         // l.13
+                    i = j + 2 * p.q - p.m;                     // l.7 (> 0)
+                    if (j >= i) walk = true;                   // l.8
+                    else complete = true;                      // m < 2q: while-else (R7)
+                }
+            } else {                                           // l.9-13
+                j -= p.q;
+                v = vv;
+                if (((z >> (v & (kWordBits - 1))) & 1u) == 0) {
+                    walk = false;                              // l.12 break
+                    j += p.S;                                  // l.18
+                } else {
+                    z = sF[v];                                 // l.13
                     if (j < i) {
                         walk = false;
                         complete = true;
                     }
                 }
             }
-            if (complete) {                            // l.14-18, index per R1
-                if (v == p.hv && verify(txt, sx, e + 1 - p.m, p.m)) {
-                    found = true;
-                    fpos = e + 1 - p.m;
-                }
-                j = e + 1;                             // (i - q) + (m - q + 1)
+            if (complete) {                                    // l.14-16, index per R1
+                need_v = v == p.hv;
+                j = e + 1;
             }
             if (!walk && j >= b) active = false;
         }
-        if (COUNT_ONLY) {
-            nfound += found ? 1u : 0u;
-        } else {
-            wo.push(found, fpos, p, lane);
+        bool found = false;
+        if (p.m > kCoopVerifyMin) {
+            uint32_t vm = __ballot_sync(HC_FULL, need_v);
+            while (vm) {
+                const uint32_t L = __ffs(vm) - 1;
+                vm &= vm - 1;
+                const uint32_t st = __shfl_sync(HC_FULL, e + 1 - p.m, L);
+                const bool ok = verify_warp(txt, sx, st, p.m, lane);
+                if (lane == L) found = ok;
+            }
+        } else if (need_v) {
+            found = verify(txt, sx, e + 1 - p.m, p.m);
         }
+        wo.push(found, e + 1 - p.m, p, lane);                 // l.17
+    }
+}
+
+// Phase A over lattice points [seg_lo, seg_hi): filter, queue survivors, run phase B
+// whenever 32 are queued.  Warp-synchronous; `qcnt` is warp-uniform.
+template <int Q, int SH, class T>
+__device__ __forceinline__ void filter_range(const KParams &p, const T &txt, const uint32_t *sF,
+                                             const uint8_t *sx, uint32_t seg_lo,
+                                             uint32_t seg_hi, uint32_t *queue, uint32_t &qcnt,
+                                             WarpOut &wo, uint32_t lane) {
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t k0 = seg_lo; k0 < seg_hi; k0 += 32 * kUnroll) {
+        uint64_t W[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t k = k0 + u * 32 + lane;
+            W[u] = k < seg_hi ? end8<Q>(txt, p.m - 1 + k * p.S) : 0ull;
+        }
+        bool pass[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t k = k0 + u * 32 + lane;
+            pass[u] = k < seg_hi && sF[qhash<Q, SH>(W[u], p.mask)] != 0u;   // l.4-6
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
+            if (bm) {
+                if (pass[u]) queue[qcnt + __popc(bm & lt)] = k0 + u * 32 + lane;
+                qcnt += __popc(bm);
+                if (qcnt >= 32) {
+                    __syncwarp();
+                    run_survivors<Q, SH>(p, txt, sF, sx, queue, 32, wo, lane);
+                    const uint32_t rest = qcnt - 32;
+                    const uint32_t nv = lane < rest ? queue[32 + lane] : 0u;
+                    __syncwarp();
+                    if (lane < rest) queue[lane] = nv;
+                    __syncwarp();
+                    qcnt = rest;
+                }
+            }
+        }
+    }
+}
+
+template <int Q, int SH, class T>
+__device__ __forceinline__ void drain(const KParams &p, const T &txt, const uint32_t *sF,
+                                      const uint8_t *sx, uint32_t *queue, uint32_t &qcnt,
+                                      WarpOut &wo, uint32_t lane) {
+    if (qcnt) {
+        __syncwarp();
+        run_survivors<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);
+        qcnt = 0;
     }
 }
 
 // ------------------------------------------------------------------ shared layout
 struct StagedLayout {
-    uint32_t f_off, x_off, wbuf_off, mbar_off, stage_off, total;
+    uint32_t f_off, x_off, q_off, wbuf_off, mbar_off, stage_off, total;
 };
 __host__ __device__ inline uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m,
@@ -273,21 +457,23 @@ __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m
     StagedLayout L;
     L.f_off = 0;
     L.x_off = round_up((1u << alpha) * 4u, 16);
-    L.wbuf_off = L.x_off + round_up(m + 8, 16);
+    L.q_off = L.x_off + round_up(m + 8, 16);
+    L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
     L.mbar_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
     L.stage_off = round_up(L.mbar_off + stages * 8u, 128);
     L.total = L.stage_off + stages * stage_bytes;
     return L;
 }
 struct GatherLayout {
-    uint32_t f_off, x_off, wbuf_off, total;
+    uint32_t f_off, x_off, q_off, wbuf_off, total;
 };
 __host__ __device__ inline GatherLayout gather_layout(uint32_t alpha, uint32_t m,
                                                       uint32_t nwarps) {
     GatherLayout L;
     L.f_off = 0;
     L.x_off = round_up((1u << alpha) * 4u, 16);
-    L.wbuf_off = L.x_off + round_up(m + 8, 16);
+    L.q_off = L.x_off + round_up(m + 8, 16);
+    L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
     L.total = L.wbuf_off + nwarps * kWarpBuf * 4u;
     return L;
 }
@@ -301,7 +487,13 @@ int gather_smem_bytes(uint32_t alpha, uint32_t m) {
 
 __device__ __forceinline__ void load_table(const KParams &p, uint32_t *sF, uint8_t *sx) {
     const uint32_t nF = 1u << p.alpha;
-    for (uint32_t w = threadIdx.x; w < nF; w += blockDim.x) sF[w] = __ldg(p.F + w);
+    if (nF >= 4) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.F);
+        uint4 *dst = reinterpret_cast<uint4 *>(sF);
+        for (uint32_t w = threadIdx.x; w < nF / 4; w += blockDim.x) dst[w] = __ldg(src + w);
+    } else {
+        for (uint32_t w = threadIdx.x; w < nF; w += blockDim.x) sF[w] = __ldg(p.F + w);
+    }
     for (uint32_t k = threadIdx.x; k < p.m; k += blockDim.x) sx[k] = __ldg(p.x + k);
     // zero the 8-byte tail so 8-byte compares of x never read uninitialised bytes
     if (threadIdx.x < 8) sx[p.m + threadIdx.x] = 0;
@@ -344,7 +536,7 @@ __device__ __forceinline__ void issue_tile(const KParams &p, uint32_t t, uint8_t
     }
 }
 
-template <int Q, bool COUNT_ONLY>
+template <int Q, int SH>
 __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kStagedThreads / 32;
@@ -367,8 +559,9 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p)
             if (t < p.ntiles) issue_tile(p, t, stages + st * p.stage_bytes, &mbar[st]);
         }
     }
+    uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
+    uint32_t qcnt = 0;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
-    uint32_t nfound = 0;
     const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
 
     for (uint32_t it = 0;; ++it) {
@@ -395,12 +588,13 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p)
             }
             __syncthreads();
         }
-        // shared address of text byte p: smem(sbuf) + (y + p - gbase)
+        // shared offset of text byte p: (sbuf - smem) + (y + p - gbase)
         const SmemText txt{smem, static_cast<uint32_t>(sbuf - smem) + static_cast<uint32_t>(y - g.gbase)};
         const uint32_t nseg = g.k1 - g.k0;
         const uint32_t seg_lo = g.k0 + (warp * nseg) / NW;
         const uint32_t seg_hi = g.k0 + ((warp + 1) * nseg) / NW;
-        run_segments<Q, COUNT_ONLY>(p, txt, sF, sx, seg_lo, seg_hi, wo, nfound, lane);
+        filter_range<Q, SH>(p, txt, sF, sx, seg_lo, seg_hi, queue, qcnt, wo, lane);
+        drain<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);   // survivors read this stage
         __syncthreads();  // every warp is done with this stage
         if (tid == 0) {
             const uint32_t tn = t + p.stages * gridDim.x;
@@ -410,15 +604,10 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p)
             }
         }
     }
-    if (COUNT_ONLY) {
-        for (int o = 16; o > 0; o >>= 1) nfound += __shfl_xor_sync(HC_FULL, nfound, o);
-        if (lane == 0 && nfound) atomicAdd(p.counter, nfound);
-    } else {
-        wo.flush(p, lane);
-    }
+    wo.flush(p, lane);
 }
 
-template <int Q, bool COUNT_ONLY>
+template <int Q, int SH>
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kGatherThreads / 32;
@@ -428,34 +617,99 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     load_table(p, sF, sx);
     __syncthreads();
+    uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
+    uint32_t qcnt = 0;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
-    uint32_t nfound = 0;
     const GlobalText txt{p.y};
     const uint32_t total_warps = gridDim.x * NW;
     for (uint32_t c = blockIdx.x * NW + warp; c < p.nchunks; c += total_warps) {
         const uint32_t seg_lo = c * p.seg_per_chunk;
         const uint32_t seg_hi = min(seg_lo + p.seg_per_chunk, p.K);
-        run_segments<Q, COUNT_ONLY>(p, txt, sF, sx, seg_lo, seg_hi, wo, nfound, lane);
+        filter_range<Q, SH>(p, txt, sF, sx, seg_lo, seg_hi, queue, qcnt, wo, lane);
     }
-    if (COUNT_ONLY) {
-        for (int o = 16; o > 0; o >>= 1) nfound += __shfl_xor_sync(HC_FULL, nfound, o);
-        if (lane == 0 && nfound) atomicAdd(p.counter, nfound);
-    } else {
-        wo.flush(p, lane);
-    }
+    drain<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);
+    wo.flush(p, lane);
 }
 
 // ------------------------------------------------------------------ launchers
-template <class K>
-static cudaError_t launch_common(K kern, const KParams &p, int threads, int smem, int work_units,
-                                 int max_ctas, cudaStream_t st, LaunchInfo *li) {
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-    if (err != cudaSuccess) return err;
+using KernFn = void (*)(const KParams);
+
+// (q, s) -> kernel instantiation.  s = floor(alpha/q) <= 15/q; for q = 1 the hash
+// is the byte itself and s plays no role.
+template <template <int, int> class Pick>
+static KernFn pick(uint32_t q, uint32_t s) {
+#define HC_C(Q, SH) \
+    if (q == Q && s == SH) return Pick<Q, SH>::fn();
+    if (q == 1) return Pick<1, 0>::fn();
+    HC_C(2, 0) HC_C(2, 1) HC_C(2, 2) HC_C(2, 3) HC_C(2, 4) HC_C(2, 5) HC_C(2, 6) HC_C(2, 7)
+    HC_C(3, 0) HC_C(3, 1) HC_C(3, 2) HC_C(3, 3) HC_C(3, 4) HC_C(3, 5)
+    HC_C(4, 0) HC_C(4, 1) HC_C(4, 2) HC_C(4, 3)
+    HC_C(5, 0) HC_C(5, 1) HC_C(5, 2) HC_C(5, 3)
+    HC_C(6, 0) HC_C(6, 1) HC_C(6, 2)
+    HC_C(7, 0) HC_C(7, 1) HC_C(7, 2)
+    HC_C(8, 0) HC_C(8, 1)
+#undef HC_C
+    return nullptr;
+}
+template <int Q, int SH>
+struct PickStaged {
+    static KernFn fn() { return staged_kernel<Q, SH>; }
+};
+template <int Q, int SH>
+struct PickGather {
+    static KernFn fn() { return gather_kernel<Q, SH>; }
+};
+
+struct KernCache {
+    KernFn fn;
+    int smem;
+    int occ;
+};
+
+static cudaError_t launch_common(KernFn kern, const KParams &p, int threads, int smem,
+                                 int work_units, int max_ctas, cudaStream_t st, LaunchInfo *li) {
+    // per-thread caches of the driver queries (they cost more than a whole large-m
+    // search): the dynamic shared-memory limit is raised once per kernel to the
+    // device maximum (so any later smem size is allowed), occupancy per (kernel, smem)
+    static thread_local KernFn attr_set[128];
+    static thread_local int nattr = 0;
+    static thread_local KernCache cache[256];
+    static thread_local int ncache = 0;
+    static thread_local int sms = 0, smem_max = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    bool have_attr = false;
+    for (int c = 0; c < nattr; ++c) have_attr |= attr_set[c] == kern;
+    if (!have_attr) {
+        cudaFuncAttributes fa;
+        cudaError_t err = cudaFuncGetAttributes(&fa, kern);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_max - static_cast<int>(fa.sharedSizeBytes));
+        if (err != cudaSuccess) {
+            if (std::getenv("HC_DEBUG"))
+                std::fprintf(stderr, "libhc: cudaFuncSetAttribute: %s\n", cudaGetErrorName(err));
+            return err;
+        }
+        if (nattr < 128) attr_set[nattr++] = kern;
+    }
+    if (smem > smem_max) return cudaErrorInvalidValue;
+    int occ = -1;
+    for (int c = 0; c < ncache; ++c)
+        if (cache[c].fn == kern && cache[c].smem == smem) occ = cache[c].occ;
+    if (occ < 0) {
+        cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (err != cudaSuccess) {
+            if (std::getenv("HC_DEBUG"))
+                std::fprintf(stderr, "libhc: occupancy(smem=%d): %s\n", smem, cudaGetErrorName(err));
+            return err;
+        }
+        if (ncache < 256) cache[ncache++] = KernCache{kern, smem, occ};
+    }
     if (occ < 1) return cudaErrorInvalidConfiguration;
     long grid = static_cast<long>(sms) * occ;
     if (grid > work_units) grid = work_units;
@@ -470,31 +724,16 @@ static cudaError_t launch_common(K kern, const KParams &p, int threads, int smem
     return cudaGetLastError();
 }
 
-#define HC_DISPATCH_Q(Q_, KERNEL, CO)                                          \
-    switch (Q_) {                                                              \
-        case 1: kern = CO ? KERNEL<1, true> : KERNEL<1, false>; break;         \
-        case 2: kern = CO ? KERNEL<2, true> : KERNEL<2, false>; break;         \
-        case 3: kern = CO ? KERNEL<3, true> : KERNEL<3, false>; break;         \
-        case 4: kern = CO ? KERNEL<4, true> : KERNEL<4, false>; break;         \
-        case 5: kern = CO ? KERNEL<5, true> : KERNEL<5, false>; break;         \
-        case 6: kern = CO ? KERNEL<6, true> : KERNEL<6, false>; break;         \
-        case 7: kern = CO ? KERNEL<7, true> : KERNEL<7, false>; break;         \
-        case 8: kern = CO ? KERNEL<8, true> : KERNEL<8, false>; break;         \
-        default: return cudaErrorInvalidValue;                                 \
-    }
-
 cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li) {
-    void (*kern)(const KParams) = nullptr;
-    const bool co = p.out == nullptr;
-    HC_DISPATCH_Q(p.q, staged_kernel, co);
+    KernFn kern = pick<PickStaged>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
     const int smem = staged_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages);
     return launch_common(kern, p, kStagedThreads, smem, static_cast<int>(p.ntiles), max_ctas, st, li);
 }
 
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li) {
-    void (*kern)(const KParams) = nullptr;
-    const bool co = p.out == nullptr;
-    HC_DISPATCH_Q(p.q, gather_kernel, co);
+    KernFn kern = pick<PickGather>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
     const int smem = gather_smem_bytes(p.alpha, p.m);
     const int warps_needed = static_cast<int>(p.nchunks);
     const int ctas = (warps_needed + kGatherThreads / 32 - 1) / (kGatherThreads / 32);
@@ -507,15 +746,31 @@ __global__ void widen_kernel(const uint32_t *src, int64_t *dst, uint32_t k) {
         dst[i] = static_cast<int64_t>(src[i]);
 }
 
-constexpr uint32_t kSmallSort = 8192;
 
-// One-CTA bitonic sort of <= kSmallSort distinct keys in shared memory.
-__global__ void __launch_bounds__(1024) small_sort_kernel(const uint32_t *src, uint32_t count,
-                                                          int64_t *dst, uint32_t k) {
+// Runs right after the search kernel, one CTA: publishes the count to the host
+// (mapped pinned word), resets the device counter for the next call, and when
+// 1 <= count <= kSmallSort orders the positions in shared memory (bitonic sort of
+// distinct keys) and writes the first min(count, max_out) as int64.
+__global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const uint32_t *pos,
+                                                      uint32_t cap, int64_t *dst,
+                                                      uint32_t max_out,
+                                                      volatile uint32_t *host_count) {
     __shared__ uint32_t s[kSmallSort];
+    const uint32_t count = *counter;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *host_count = count;
+        *counter = 0;
+    }
+    if (dst == nullptr || max_out == 0 || count == 0 || count > cap || count > kSmallSort) return;
+    const uint32_t k = min(count, max_out);
+    if (count == 1) {
+        if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(pos[0]);
+        return;
+    }
     uint32_t P = 1;
     while (P < count) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < count ? src[i] : 0xffffffffu;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < count ? pos[i] : 0xffffffffu;
     __syncthreads();
     for (uint32_t size = 2; size <= P; size <<= 1) {
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
@@ -536,38 +791,35 @@ __global__ void __launch_bounds__(1024) small_sort_kernel(const uint32_t *src, u
     for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) dst[i] = static_cast<int64_t>(s[i]);
 }
 
-cudaError_t sort_and_widen(uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
-                           uint32_t k, cudaStream_t st, int *launches) {
-    if (k == 0) return cudaSuccess;
-    if (count <= 1) {
-        widen_kernel<<<1, 32, 0, st>>>(pos, dst, k);
-        if (launches) ++*launches;
-        return cudaGetLastError();
-    }
-    if (count <= kSmallSort) {
-        small_sort_kernel<<<1, 1024, 0, st>>>(pos, count, dst, k);
-        if (launches) ++*launches;
-        return cudaGetLastError();
-    }
+cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
+                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st) {
+    finish_kernel<<<1, 1024, 0, st>>>(counter, pos, cap, dst, max_out, host_count_dev);
+    return cudaGetLastError();
+}
+
+// count > kSmallSort: CUB radix sort on ceil(log2 n) bits, then widen the first k.
+cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
+                       uint32_t k, cudaStream_t st, int *launches) {
     int end_bit = 1;
     while (end_bit < 32 && (static_cast<uint64_t>(1) << end_bit) <= n_bound) ++end_bit;
     uint32_t *alt = nullptr;
-    void *tmp = nullptr;
     size_t tmp_bytes = 0;
     cudaError_t err = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, pos, alt,
                                                      static_cast<int>(count), 0, end_bit, st);
     if (err != cudaSuccess) return err;
-    err = cudaMallocAsync(reinterpret_cast<void **>(&alt), static_cast<size_t>(count) * 4 + tmp_bytes + 256, st);
+    err = cudaMallocAsync(reinterpret_cast<void **>(&alt),
+                          static_cast<size_t>(count) * 4 + tmp_bytes + 256, st);
     if (err != cudaSuccess) return err;
-    tmp = reinterpret_cast<void *>(
-        (reinterpret_cast<uintptr_t>(alt) + static_cast<size_t>(count) * 4 + 255) & ~static_cast<uintptr_t>(255));
+    void *tmp = reinterpret_cast<void *>(
+        (reinterpret_cast<uintptr_t>(alt) + static_cast<size_t>(count) * 4 + 255) &
+        ~static_cast<uintptr_t>(255));
     err = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, pos, alt, static_cast<int>(count), 0,
                                          end_bit, st);
     if (err == cudaSuccess) {
         const uint32_t blocks = min((k + 255) / 256, 148u * 8u);
         widen_kernel<<<blocks, 256, 0, st>>>(alt, dst, k);
         err = cudaGetLastError();
-        if (launches) *launches += 4;  // CUB onesweep: histogram + passes; approximate
+        if (launches) *launches += 1 + (end_bit + 7) / 8 + 1;  // histogram + onesweep passes + widen
     }
     cudaError_t e2 = cudaFreeAsync(alt, st);
     return err != cudaSuccess ? err : e2;

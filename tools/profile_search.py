@@ -1,0 +1,49 @@
+#!/usr/bin/env python
+"""Run a few hc_search calls of one config / m (for ncu captures and quick timing).
+
+    python tools/profile_search.py --config C2 --m 16 32 1024 --reps 3 [--path 0|1|2]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2310_15711_b200 import hc  # noqa: E402
+from paper_2310_15711_b200 import inputs as I  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--m", type=int, nargs="+", default=[16])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--path", type=int, default=0)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--spl", type=int, default=0)
+    args = ap.parse_args()
+    cfg = I.CONFIGS[args.config]
+    y, block = I.config_text(cfg, args.n)
+    yd = torch.from_numpy(y).cuda()
+    flush = torch.empty(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8,
+                        device="cuda")
+    for m in args.m:
+        q, a = cfg.qa[m]
+        o, x = I.patterns(cfg, y, m, count=1, block=block)[0]
+        h = hc.prepare(x, q, a)
+        for r in range(args.reps):
+            flush.zero_()
+            res, st = hc.search(h, yd, stats=True, path=args.path, tile_bytes=args.tile,
+                                stages=args.stages, seg_per_lane=args.spl, time_kernel=1)
+            torch.cuda.synchronize()
+            print(f"m={m} q={q} a={a} rep={r} count={len(res)} kernel_us={st['kernel_ms']*1e3:.1f} "
+                  f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} {st}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
