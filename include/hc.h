@@ -99,6 +99,10 @@ typedef struct hc_search_opts {
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
     int time_kernel;  /* 1: record CUDA events around the search kernel (stats->kernel_ms) */
+    int ctas_per_sm;  /* cap on resident CTAs per SM for the persistent grid (0 = occupancy max) */
+    int debug;        /* 0; 1 = staged path streams the tiles but skips the search (measures
+                         the TMA pipeline alone; results are NOT valid) */
+    int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage) */
 } hc_search_opts;
 
 typedef struct hc_search_stats {

@@ -292,6 +292,8 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     p.S = S;
     p.alpha = h->alpha;
     p.K = K;
+    p.debug = static_cast<uint32_t>(o.debug);
+    p.tma_chunk = o.tma_chunk > 0 ? (static_cast<uint32_t>(o.tma_chunk) + 15) & ~15u : 0u;
 
     int path = o.path;
     if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STAGED : HC_PATH_GATHER;
@@ -345,8 +347,8 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             cudaEventRecord(ev0, stream);
         }
         const char *stage = "search kernel launch";
-        e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, &li)
-                                   : hc::launch_gather(p, stream, o.max_ctas, &li);
+        e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, o.ctas_per_sm, &li)
+                                   : hc::launch_gather(p, stream, o.max_ctas, o.ctas_per_sm, &li);
         ++launches;
         if (timed) cudaEventRecord(ev1, stream);
         if (e == cudaSuccess) {

@@ -30,6 +30,8 @@ struct KParams {
     uint32_t *out;       // positions (window starts), unordered; NULL = count only
     uint32_t cap;        // capacity of out
     uint32_t *counter;   // [0] = total occurrences (may exceed cap)
+    uint32_t debug;      // 1: staged kernel skips the search (pipeline measurement only)
+    uint32_t tma_chunk;  // staged: split each tile's bulk copy into pieces of this size (0 = one)
 };
 
 struct LaunchInfo {
@@ -37,8 +39,10 @@ struct LaunchInfo {
 };
 
 // Device-side entry points (hc_kernels.cu).  All enqueue on `st`.
-cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li);
-cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li);
+cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li);
+cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li);
 // One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,
 // ordering of <= kSmallSort positions into dst (first min(count, max_out), int64).
 cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,

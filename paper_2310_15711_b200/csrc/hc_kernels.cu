@@ -46,6 +46,7 @@ constexpr uint32_t kWordBits = 32;       // w (R2)
 constexpr uint32_t kLongWalk = 12;       // walks with >= this many steps left go warp-wide
 constexpr uint32_t kCoopVerifyMin = 64;  // m above which verification is warp-wide
 constexpr int kUnroll = 4;               // lattice rounds whose loads are issued together
+constexpr uint32_t kCtaQueue = 1024;     // staged: CTA-wide survivor queue entries
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -119,17 +120,44 @@ struct GlobalText {
     static constexpr bool kLoSafe = false;  // the word before may be outside y
 };
 
-// Text byte p read from a shared-memory stage: byte p is at smem[base + p]
-// (offsets mod 2^32; the stage is 16-aligned so offsets keep y's alignment mod 16).
+// Shared-memory loads by shared-space address.  Not volatile: callers make the
+// address depend on a value produced after the mbarrier wait (see fence_value), so
+// they cannot be hoisted above it.
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+    uint64_t r;
+    asm("ld.shared.u64 %0, [%1];" : "=l"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t r;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t r;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
+// Opaque copy of v, ordered after every earlier volatile asm (e.g. an mbarrier wait).
+__device__ __forceinline__ uint32_t fence_value(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v) :: "memory");
+    return v;
+}
+
+// Text byte p read from a shared-memory stage: byte p is at shared address base + p
+// (mod 2^32; the stage is 16-aligned so addresses keep y's alignment mod 16).
 struct SmemText {
-    const uint8_t *s;  // start of the dynamic shared-memory array
     uint32_t base;
     __device__ __forceinline__ uint32_t addr(uint32_t p) const { return base + p; }
-    __device__ __forceinline__ uint64_t word(uint32_t aligned) const {
-        return *reinterpret_cast<const uint64_t *>(s + aligned);
-    }
-    __device__ __forceinline__ uint32_t byte(uint32_t p) const { return s[base + p]; }
+    __device__ __forceinline__ uint64_t word(uint32_t aligned) const { return lds64(aligned); }
+    __device__ __forceinline__ uint32_t byte(uint32_t p) const { return lds8(base + p); }
     static constexpr bool kLoSafe = true;   // stages never start at shared offset 0
+};
+
+// F (2^alpha words) in shared memory, addressed by shared-space address.
+struct FTable {
+    uint32_t base;
+    __device__ __forceinline__ uint32_t operator[](uint32_t v) const { return lds32(base + 4 * v); }
 };
 
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
@@ -232,7 +260,7 @@ __device__ __forceinline__ bool verify_warp(const T &t, const uint8_t *sx, uint3
 // the sequential loop's break (l.12).  On return j is the position of the last
 // evaluated step (the failing one if broke) and v its hash.
 template <int Q, int SH, class T>
-__device__ __forceinline__ void walk_warp(const KParams &p, const T &txt, const uint32_t *sF,
+__device__ __forceinline__ void walk_warp(const KParams &p, const T &txt, const FTable &sF,
                                           uint32_t lane, uint32_t &j, uint32_t i, uint32_t z,
                                           uint32_t &v, bool &broke) {
     uint32_t R = (j - i) / p.q + 1;  // steps while j >= i
@@ -305,7 +333,7 @@ struct WarpOut {
 
 // Phase B: HC (Fig. 5) on `cnt` <= 32 queued segments, one per lane.  Warp-synchronous.
 template <int Q, int SH, class T>
-__device__ __noinline__ void run_survivors(const KParams &p, const T &txt, const uint32_t *sF,
+__device__ __forceinline__ void run_survivors(const KParams &p, const T &txt, const FTable &sF,
                                            const uint8_t *sx, const uint32_t *queue,
                                            uint32_t cnt, WarpOut &wo, uint32_t lane) {
     bool active = lane < cnt;
@@ -393,50 +421,107 @@ __device__ __noinline__ void run_survivors(const KParams &p, const T &txt, const
     }
 }
 
-// Phase A over lattice points [seg_lo, seg_hi): filter, queue survivors, run phase B
-// whenever 32 are queued.  Warp-synchronous; `qcnt` is warp-uniform.
-template <int Q, int SH, class T>
-__device__ __forceinline__ void filter_range(const KParams &p, const T &txt, const uint32_t *sF,
-                                             const uint8_t *sx, uint32_t seg_lo,
-                                             uint32_t seg_hi, uint32_t *queue, uint32_t &qcnt,
-                                             WarpOut &wo, uint32_t lane) {
-    const uint32_t lt = lanemask_lt();
-    for (uint32_t k0 = seg_lo; k0 < seg_hi; k0 += 32 * kUnroll) {
+// Phase A over lattice points [seg_lo, seg_hi), 32 * kUnroll per warp step: every
+// lane hashes the q-gram ending at its lattice point a_k = m-1 + k S (Fig. 5 l.4)
+// and tests F[v] != 0 (l.6).  Survivor segments are handed to `sink` (warp-uniform
+// call, ballot mask + the lane's k).  Full steps run without bounds checks.
+template <int Q, int SH, class T, class Sink>
+__device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, const FTable &sF,
+                                               uint32_t seg_lo, uint32_t seg_hi, uint32_t lane,
+                                               Sink &&sink) {
+    const uint32_t step = 32 * p.S;
+    uint32_t pos = p.m - 1 + (seg_lo + lane) * p.S;   // window end of lattice point seg_lo+lane
+    uint32_t k0 = seg_lo;
+    for (; k0 + 32 * kUnroll <= seg_hi; k0 += 32 * kUnroll, pos += kUnroll * step) {
         uint64_t W[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint32_t k = k0 + u * 32 + lane;
-            W[u] = k < seg_hi ? end8<Q>(txt, p.m - 1 + k * p.S) : 0ull;
-        }
+        for (int u = 0; u < kUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
         bool pass[kUnroll];
+        bool any = false;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            const uint32_t k = k0 + u * 32 + lane;
-            pass[u] = k < seg_hi && sF[qhash<Q, SH>(W[u], p.mask)] != 0u;   // l.4-6
+            pass[u] = sF[qhash<Q, SH>(W[u], p.mask)] != 0u;
+            any |= pass[u];
         }
+        if (__any_sync(HC_FULL, any)) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
-            if (bm) {
-                if (pass[u]) queue[qcnt + __popc(bm & lt)] = k0 + u * 32 + lane;
-                qcnt += __popc(bm);
-                if (qcnt >= 32) {
-                    __syncwarp();
-                    run_survivors<Q, SH>(p, txt, sF, sx, queue, 32, wo, lane);
-                    const uint32_t rest = qcnt - 32;
-                    const uint32_t nv = lane < rest ? queue[32 + lane] : 0u;
-                    __syncwarp();
-                    if (lane < rest) queue[lane] = nv;
-                    __syncwarp();
-                    qcnt = rest;
-                }
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
+                if (bm) sink(bm, pass[u], k0 + u * 32 + lane);
             }
         }
     }
+    for (; k0 < seg_hi; k0 += 32, pos += step) {       // ragged tail, one round at a time
+        const bool in = k0 + lane < seg_hi;
+        const bool pass = in && sF[qhash<Q, SH>(end8<Q>(txt, pos), p.mask)] != 0u;
+        const uint32_t bm = __ballot_sync(HC_FULL, pass);
+        if (bm) sink(bm, pass, k0 + lane);
+    }
 }
 
+// Gather path sink: per-warp queue, phase B whenever 32 are queued (survivors read
+// global memory, so the queue may span chunks).
 template <int Q, int SH, class T>
-__device__ __forceinline__ void drain(const KParams &p, const T &txt, const uint32_t *sF,
+struct WarpQueueSink {
+    const KParams &p;
+    const T &txt;
+    const FTable &sF;
+    const uint8_t *sx;
+    uint32_t *queue;
+    uint32_t &qcnt;
+    WarpOut &wo;
+    uint32_t lane;
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
+        if (pass) queue[qcnt + __popc(bm & lanemask_lt())] = k;
+        qcnt += __popc(bm);
+        if (qcnt >= 32) {
+            __syncwarp();
+            run_survivors<Q, SH>(p, txt, sF, sx, queue, 32, wo, lane);
+            const uint32_t rest = qcnt - 32;
+            const uint32_t nv = lane < rest ? queue[32 + lane] : 0u;
+            __syncwarp();
+            if (lane < rest) queue[lane] = nv;
+            __syncwarp();
+            qcnt = rest;
+        }
+    }
+};
+
+// Staged path sink: a CTA-wide queue, so that phase B runs after the tile's filter in
+// full batches of 32 (one partial batch per tile, not one per warp).  If the CTA
+// queue is full the warp runs the overflow itself.
+template <int Q, int SH, class T>
+struct CtaQueueSink {
+    const KParams &p;
+    const T &txt;
+    const FTable &sF;
+    const uint8_t *sx;
+    uint32_t *cq;
+    uint32_t *cq_count;
+    uint32_t *wq;
+    WarpOut &wo;
+    uint32_t lane;
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
+        const uint32_t nb = __popc(bm);
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(cq_count, nb);
+        base = __shfl_sync(HC_FULL, base, 0);
+        const uint32_t r = __popc(bm & lanemask_lt());
+        if (base + nb <= kCtaQueue) {
+            if (pass) cq[base + r] = k;
+        } else {
+            const bool local = pass && base + r >= kCtaQueue;
+            if (pass && !local) cq[base + r] = k;
+            const uint32_t lm = __ballot_sync(HC_FULL, local);
+            if (local) wq[__popc(lm & lanemask_lt())] = k;
+            __syncwarp();
+            run_survivors<Q, SH>(p, txt, sF, sx, wq, __popc(lm), wo, lane);
+        }
+    }
+};
+
+template <int Q, int SH, class T>
+__device__ __forceinline__ void drain(const KParams &p, const T &txt, const FTable &sF,
                                       const uint8_t *sx, uint32_t *queue, uint32_t &qcnt,
                                       WarpOut &wo, uint32_t lane) {
     if (qcnt) {
@@ -448,7 +533,7 @@ __device__ __forceinline__ void drain(const KParams &p, const T &txt, const uint
 
 // ------------------------------------------------------------------ shared layout
 struct StagedLayout {
-    uint32_t f_off, x_off, q_off, wbuf_off, mbar_off, stage_off, total;
+    uint32_t f_off, x_off, q_off, wbuf_off, cq_off, cnt_off, mbar_off, stage_off, total;
 };
 __host__ __device__ inline uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m,
@@ -459,7 +544,9 @@ __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m
     L.x_off = round_up((1u << alpha) * 4u, 16);
     L.q_off = L.x_off + round_up(m + 8, 16);
     L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
-    L.mbar_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    L.cq_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    L.cnt_off = L.cq_off + kCtaQueue * 4u;
+    L.mbar_off = L.cnt_off + 16u;
     L.stage_off = round_up(L.mbar_off + stages * 8u, 128);
     L.total = L.stage_off + stages * stage_bytes;
     return L;
@@ -529,8 +616,10 @@ __device__ __forceinline__ void issue_tile(const KParams &p, uint32_t t, uint8_t
     if (g.B > g.A) {
         const uint32_t bytes = static_cast<uint32_t>(g.B - g.A);
         mbar_arrive_expect_tx(bar, bytes);
-        bulk_g2s(smem_u32(stage) + static_cast<uint32_t>(g.A - g.gbase),
-                 reinterpret_cast<const void *>(g.A), bytes, bar);
+        const uint32_t chunk = p.tma_chunk ? p.tma_chunk : bytes;
+        for (uint32_t o = 0; o < bytes; o += chunk)
+            bulk_g2s(smem_u32(stage) + static_cast<uint32_t>(g.A - g.gbase) + o,
+                     reinterpret_cast<const void *>(g.A + o), min(chunk, bytes - o), bar);
     } else {
         mbar_arrive(bar);
     }
@@ -541,16 +630,19 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p)
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kStagedThreads / 32;
     const StagedLayout L = staged_layout(p.alpha, p.m, p.stage_bytes, p.stages, NW);
-    uint32_t *sF = reinterpret_cast<uint32_t *>(smem + L.f_off);
+    uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L.mbar_off);
     uint8_t *stages = smem + L.stage_off;
+    uint32_t *cq = reinterpret_cast<uint32_t *>(smem + L.cq_off);
+    uint32_t *cq_count = reinterpret_cast<uint32_t *>(smem + L.cnt_off);  // [2], by tile parity
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    load_table(p, sF, sx);
+    load_table(p, sFp, sx);
     if (tid == 0) {
         for (uint32_t st = 0; st < p.stages; ++st) mbar_init(&mbar[st], 1);
         fence_mbar_init();
+        cq_count[0] = cq_count[1] = 0;
     }
     __syncthreads();
     if (tid == 0) {
@@ -559,49 +651,70 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p)
             if (t < p.ntiles) issue_tile(p, t, stages + st * p.stage_bytes, &mbar[st]);
         }
     }
+    const FTable sF{smem_u32(sFp)};
     uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
-    uint32_t qcnt = 0;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
+    const uint32_t y32 = static_cast<uint32_t>(y);
+    const uint32_t stage0 = smem_u32(stages);
 
+    uint32_t st = 0, par = 0;
     for (uint32_t it = 0;; ++it) {
         const uint32_t t = blockIdx.x + it * gridDim.x;
         if (t >= p.ntiles) break;
-        const uint32_t st = it % p.stages;
-        const uint32_t par = (it / p.stages) & 1u;
         uint8_t *sbuf = stages + st * p.stage_bytes;
-        const TileGeom g = tile_geom(p, t);
+        const uint32_t k0 = t * p.seg_per_tile;
+        const uint32_t k1 = min(k0 + p.seg_per_tile, p.K);
+        const uint32_t lo = k0 * p.S;                       // first text byte of the tile
         mbar_wait(&mbar[st], par);
-        // bytes of the tile outside the bulk-copied 16-aligned interior (only at the
-        // two ends of an unaligned text, or for tiny texts): plain byte loads
-        const uintptr_t ga = y + g.lo, gh = y + g.hi;
-        const bool edges = (g.B <= g.A) || (g.A > ga) || (g.B < gh);
-        if (edges) {
-            if (g.B <= g.A) {
-                for (uintptr_t a = ga + tid; a < gh; a += blockDim.x)
-                    sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
-            } else {
-                for (uintptr_t a = ga + tid; a < g.A; a += blockDim.x)
-                    sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
-                for (uintptr_t a = g.B + tid; a < gh; a += blockDim.x)
-                    sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+        // tiles at the two text ends may hold bytes outside the 16-aligned interior the
+        // bulk copy moved (unaligned y, tiny texts): plain byte loads for those
+        if (t == 0 || t + 2 >= p.ntiles) {
+            const TileGeom g = tile_geom(p, t);
+            const uintptr_t ga = y + g.lo, gh = y + g.hi;
+            const bool edges = (g.B <= g.A) || (g.A > ga) || (g.B < gh);
+            if (edges) {
+                if (g.B <= g.A) {
+                    for (uintptr_t a = ga + tid; a < gh; a += blockDim.x)
+                        sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+                } else {
+                    for (uintptr_t a = ga + tid; a < g.A; a += blockDim.x)
+                        sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+                    for (uintptr_t a = g.B + tid; a < gh; a += blockDim.x)
+                        sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+                }
             }
             __syncthreads();
         }
-        // shared offset of text byte p: (sbuf - smem) + (y + p - gbase)
-        const SmemText txt{smem, static_cast<uint32_t>(sbuf - smem) + static_cast<uint32_t>(y - g.gbase)};
-        const uint32_t nseg = g.k1 - g.k0;
-        const uint32_t seg_lo = g.k0 + (warp * nseg) / NW;
-        const uint32_t seg_hi = g.k0 + ((warp + 1) * nseg) / NW;
-        filter_range<Q, SH>(p, txt, sF, sx, seg_lo, seg_hi, queue, qcnt, wo, lane);
-        drain<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);   // survivors read this stage
-        __syncthreads();  // every warp is done with this stage
+        // shared address of text byte p: stage + ((y + lo) & 15) + (p - lo)
+        const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
+        const uint32_t nseg = k1 - k0;
+        const uint32_t seg_lo = k0 + (warp * nseg) / NW;
+        const uint32_t seg_hi = k0 + ((warp + 1) * nseg) / NW;
+        uint32_t *cnt = cq_count + (it & 1u);
+        if (p.debug == 0) {
+            CtaQueueSink<Q, SH, SmemText> sink{p, txt, sF, sx, cq, cnt, queue, wo, lane};
+            filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
+        }
+        __syncthreads();
+        // phase B in full batches of 32 spread over the warps; the other parity's
+        // counter (last read in the previous tile) is reset for the next tile
+        const uint32_t total = min(*cnt, kCtaQueue);
+        if (tid == 0) cq_count[(it & 1u) ^ 1u] = 0;
+        const uint32_t nbatch = (total + 31) / 32;
+        for (uint32_t bt = (warp + it) % NW; bt < nbatch; bt += NW)
+            run_survivors<Q, SH>(p, txt, sF, sx, cq + 32 * bt, min(32u, total - 32 * bt), wo, lane);
+        __syncthreads();  // every warp is done with this stage and with cq
         if (tid == 0) {
             const uint32_t tn = t + p.stages * gridDim.x;
             if (tn < p.ntiles) {
                 fence_proxy_async();
                 issue_tile(p, tn, sbuf, &mbar[st]);
             }
+        }
+        if (++st == p.stages) {
+            st = 0;
+            par ^= 1u;
         }
     }
     wo.flush(p, lane);
@@ -612,20 +725,22 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kGatherThreads / 32;
     const GatherLayout L = gather_layout(p.alpha, p.m, NW);
-    uint32_t *sF = reinterpret_cast<uint32_t *>(smem + L.f_off);
+    uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    load_table(p, sF, sx);
+    load_table(p, sFp, sx);
     __syncthreads();
+    const FTable sF{fence_value(smem_u32(sFp))};
     uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
     uint32_t qcnt = 0;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const GlobalText txt{p.y};
+    WarpQueueSink<Q, SH, GlobalText> sink{p, txt, sF, sx, queue, qcnt, wo, lane};
     const uint32_t total_warps = gridDim.x * NW;
     for (uint32_t c = blockIdx.x * NW + warp; c < p.nchunks; c += total_warps) {
         const uint32_t seg_lo = c * p.seg_per_chunk;
         const uint32_t seg_hi = min(seg_lo + p.seg_per_chunk, p.K);
-        filter_range<Q, SH>(p, txt, sF, sx, seg_lo, seg_hi, queue, qcnt, wo, lane);
+        filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
     }
     drain<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);
     wo.flush(p, lane);
@@ -667,7 +782,8 @@ struct KernCache {
 };
 
 static cudaError_t launch_common(KernFn kern, const KParams &p, int threads, int smem,
-                                 int work_units, int max_ctas, cudaStream_t st, LaunchInfo *li) {
+                                 int work_units, int max_ctas, int ctas_per_sm, cudaStream_t st,
+                                 LaunchInfo *li) {
     // per-thread caches of the driver queries (they cost more than a whole large-m
     // search): the dynamic shared-memory limit is raised once per kernel to the
     // device maximum (so any later smem size is allowed), occupancy per (kernel, smem)
@@ -711,6 +827,7 @@ static cudaError_t launch_common(KernFn kern, const KParams &p, int threads, int
         if (ncache < 256) cache[ncache++] = KernCache{kern, smem, occ};
     }
     if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (ctas_per_sm > 0 && occ > ctas_per_sm) occ = ctas_per_sm;
     long grid = static_cast<long>(sms) * occ;
     if (grid > work_units) grid = work_units;
     if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
@@ -724,20 +841,23 @@ static cudaError_t launch_common(KernFn kern, const KParams &p, int threads, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li) {
+cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li) {
     KernFn kern = pick<PickStaged>(p.q, p.s);
     if (!kern) return cudaErrorInvalidValue;
     const int smem = staged_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages);
-    return launch_common(kern, p, kStagedThreads, smem, static_cast<int>(p.ntiles), max_ctas, st, li);
+    return launch_common(kern, p, kStagedThreads, smem, static_cast<int>(p.ntiles), max_ctas,
+                         ctas_per_sm, st, li);
 }
 
-cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, LaunchInfo *li) {
+cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li) {
     KernFn kern = pick<PickGather>(p.q, p.s);
     if (!kern) return cudaErrorInvalidValue;
     const int smem = gather_smem_bytes(p.alpha, p.m);
     const int warps_needed = static_cast<int>(p.nchunks);
     const int ctas = (warps_needed + kGatherThreads / 32 - 1) / (kGatherThreads / 32);
-    return launch_common(kern, p, kGatherThreads, smem, ctas, max_ctas, st, li);
+    return launch_common(kern, p, kGatherThreads, smem, ctas, max_ctas, ctas_per_sm, st, li);
 }
 
 // ------------------------------------------------------------------ ordering

@@ -26,23 +26,35 @@ def main():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--spl", type=int, default=0)
+    ap.add_argument("--cps", type=int, default=0)
+    ap.add_argument("--debug", type=int, default=0)
+    ap.add_argument("--chunk", type=int, default=0)
     args = ap.parse_args()
     cfg = I.CONFIGS[args.config]
     y, block = I.config_text(cfg, args.n)
     yd = torch.from_numpy(y).cuda()
-    flush = torch.empty(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8,
-                        device="cuda")
+    flush = torch.ones(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8,
+                       device="cuda")
+    torch.cuda.synchronize()
+
+    def flush_l2():
+        # read-only flush: evicts the text with CLEAN lines (a write flush would leave
+        # dirty lines whose write-back then competes with the timed search)
+        flush.view(torch.int64).sum()
     for m in args.m:
         q, a = cfg.qa[m]
         o, x = I.patterns(cfg, y, m, count=1, block=block)[0]
         h = hc.prepare(x, q, a)
         for r in range(args.reps):
-            flush.zero_()
+            flush_l2()
             res, st = hc.search(h, yd, stats=True, path=args.path, tile_bytes=args.tile,
-                                stages=args.stages, seg_per_lane=args.spl, time_kernel=1)
+                                stages=args.stages, seg_per_lane=args.spl, time_kernel=1,
+                                ctas_per_sm=args.cps, debug=args.debug,
+                                tma_chunk=args.chunk)
             torch.cuda.synchronize()
             print(f"m={m} q={q} a={a} rep={r} count={len(res)} kernel_us={st['kernel_ms']*1e3:.1f} "
-                  f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} {st}", flush=True)
+                  f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}",
+                  flush=True)
 
 
 if __name__ == "__main__":
