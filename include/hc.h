@@ -103,6 +103,9 @@ typedef struct hc_search_opts {
     int debug;        /* 0; 1 = staged path streams the tiles but skips the search (measures
                          the TMA pipeline alone; results are NOT valid) */
     int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage) */
+    unsigned long long *trace; /* staged, debugging: DEVICE buffer of grid x trace_tiles x 4
+                                  %globaltimer stamps per (CTA, tile), or NULL */
+    int trace_tiles;
 } hc_search_opts;
 
 typedef struct hc_search_stats {
@@ -114,6 +117,7 @@ typedef struct hc_search_stats {
     int launches;      /* kernels launched by this call (search, re-run, sort, copy) */
     int reruns;        /* search re-runs after the position scratch overflowed */
     float kernel_ms;   /* search kernel time (first launch), if time_kernel */
+    uint32_t dbg[2];   /* debug == 5: phase-B loop iterations and phase-B calls */
 } hc_search_stats;
 
 /* hc_search with explicit options (NULL = defaults) and optional statistics (NULL = none). */

@@ -294,6 +294,8 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     p.K = K;
     p.debug = static_cast<uint32_t>(o.debug);
     p.tma_chunk = o.tma_chunk > 0 ? (static_cast<uint32_t>(o.tma_chunk) + 15) & ~15u : 0u;
+    p.trace = o.trace;
+    p.trace_tiles = o.trace_tiles > 0 ? static_cast<uint32_t>(o.trace_tiles) : 0u;
 
     int path = o.path;
     if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STAGED : HC_PATH_GATHER;
@@ -303,13 +305,15 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         const uint32_t need = 32 * S + m + 48;
         if (stage < need) stage = need;
         stage = (stage + 15) & ~15u;
-        p.stages = o.stages > 0 ? static_cast<uint32_t>(o.stages) : kDefaultStages;
+        // >= 2: a tile's stage is held through the next tile's filter (its survivors)
+        p.stages = o.stages > 0 ? std::max<uint32_t>(2u, static_cast<uint32_t>(o.stages))
+                                : kDefaultStages;
         p.stage_bytes = stage;
         // segments whose bytes [k0*S, m-1+k1*S) fit with 16 B of misalignment slack at
         // each end: (k1-k0)*S + m - 1 + 32 <= stage
         p.seg_per_tile = (stage - 32 - (m - 1)) / S;
         p.ntiles = (K + p.seg_per_tile - 1) / p.seg_per_tile;
-        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages);
+        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, 0, 0);
         if (smem > max_smem_optin(h->device)) {
             if (o.path == HC_PATH_STAGED) return fail(HC_EINVAL);
             path = HC_PATH_GATHER;
@@ -374,6 +378,10 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             return cuda_fail(e, stage);
         }
         count = *reinterpret_cast<volatile uint32_t *>(sc->host_count);
+        if (o.debug == 5 && stats) {
+            cudaMemcpy(stats->dbg, sc->buf + 2, 8, cudaMemcpyDeviceToHost);
+            cudaMemset(sc->buf + 2, 0, 8);
+        }
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all
             cap = count;

@@ -23,6 +23,8 @@ struct KParams {
     uint32_t ntiles;
     uint32_t stage_bytes;   // bytes per stage buffer (multiple of 16)
     uint32_t stages;
+    uint32_t slot_bytes;    // survivor box slot size (>= S + m + 30, multiple of 16)
+    uint32_t nbox;          // survivor boxes (32 slots each) per CTA
     // gather path
     uint32_t seg_per_chunk; // segments per warp chunk
     uint32_t nchunks;
@@ -32,6 +34,8 @@ struct KParams {
     uint32_t *counter;   // [0] = total occurrences (may exceed cap)
     uint32_t debug;      // 1: staged kernel skips the search (pipeline measurement only)
     uint32_t tma_chunk;  // staged: split each tile's bulk copy into pieces of this size (0 = one)
+    unsigned long long *trace;  // staged: per-(CTA, tile) %globaltimer events (debugging), or NULL
+    uint32_t trace_tiles;       // tiles per CTA recorded
 };
 
 struct LaunchInfo {
@@ -52,7 +56,8 @@ cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, in
                        uint32_t k, cudaStream_t st, int *launches);
 constexpr uint32_t kSmallSort = 8192;
 
-int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages);
+int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
+                      uint32_t slot_bytes, uint32_t nbox);
 int gather_smem_bytes(uint32_t alpha, uint32_t m);
 
 constexpr int kStagedThreads = 256;

@@ -46,7 +46,13 @@ constexpr uint32_t kWordBits = 32;       // w (R2)
 constexpr uint32_t kLongWalk = 12;       // walks with >= this many steps left go warp-wide
 constexpr uint32_t kCoopVerifyMin = 64;  // m above which verification is warp-wide
 constexpr int kUnroll = 4;               // lattice rounds whose loads are issued together
-constexpr uint32_t kCtaQueue = 1024;     // staged: CTA-wide survivor queue entries
+constexpr int kWalkUnroll = 4;           // walk steps evaluated per phase-B iteration
+constexpr uint32_t kSurvWarps = 2;       // staged: survivor/producer warps per CTA
+
+// Launch parameters, copied to shared memory at kernel start so that the out-of-line
+// phase-B routine can read them without a stack copy.
+__shared__ KParams s_params;
+constexpr uint32_t kRegion = 64;         // staged: survivor entries per filter warp per slot
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -73,7 +79,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "HC_WAIT%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
         "@P1 bra HC_DONE%=;\n\t"
         "bra HC_WAIT%=;\n"
         "HC_DONE%=:\n\t}" ::"r"(smem_u32(bar)),
@@ -88,6 +94,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
             dst),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_event(const KParams &p, uint32_t it, uint32_t ev) {
+    if (p.trace && it < p.trace_tiles)
+        p.trace[(static_cast<size_t>(blockIdx.x) * p.trace_tiles + it) * 4 + ev] = gtimer();
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
@@ -331,70 +346,106 @@ struct WarpOut {
     }
 };
 
-// Phase B: HC (Fig. 5) on `cnt` <= 32 queued segments, one per lane.  Warp-synchronous.
+// Phase B: HC (Fig. 5) on one segment per active lane (lattice point k), warp-
+// synchronous.  Each iteration a lane evaluates its window-end hash (l.4-6) and up to
+// kWalkUnroll walk steps (l.9-13): the hashes and F words of all positions it may
+// need (j, j-q, ..., never below the window) are loaded in parallel, then the link
+// tests run in registers in the paper's order, so the result is the sequential
+// loop's; one iteration costs one shared/global round trip instead of one per step.
 template <int Q, int SH, class T>
-__device__ __forceinline__ void run_survivors(const KParams &p, const T &txt, const FTable &sF,
-                                           const uint8_t *sx, const uint32_t *queue,
-                                           uint32_t cnt, WarpOut &wo, uint32_t lane) {
-    bool active = lane < cnt;
-    const uint32_t k = active ? queue[lane] : 0u;
-    __syncwarp();
+__device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF, const uint8_t *sx,
+                                                   bool active, uint32_t k, uint32_t *wbuf,
+                                                   uint32_t wcnt, uint32_t lane) {
+    // One out-of-line copy per kernel: phase B is cold relative to the filter loop and
+    // inlining it at every call site multiplied the kernel's code size (I-cache misses).
+    const KParams &p = s_params;
+    WarpOut wo{wbuf, wcnt};
+    constexpr int U = kWalkUnroll;
     uint32_t j = p.m - 1 + k * p.S;            // lattice window end a_k
     const uint32_t b = min(j + p.S, p.n);      // segment bound
-    uint32_t e = 0, i = 0, z = 0, v = 0;
+    uint32_t e = 0, i = 0, z = 0, v = 0, wsteps = 0;
     bool walk = false;
+    const bool long_walks = p.m >= 2 * kLongWalk * Q;   // warp-wide walks can pay off
+    if (p.debug == 5 && lane == 0) atomicAdd(p.counter + 3, 1u);
     while (__any_sync(HC_FULL, active)) {
+        if (p.debug == 5 && lane == 0) atomicAdd(p.counter + 2, 1u);
         bool need_v = false, stepped = false;
-        // long walks: warp-wide, one lane at a time
-        uint32_t lm = __ballot_sync(HC_FULL, active && walk && (j - i) >= kLongWalk * p.q);
-        while (lm) {
-            const uint32_t L = __ffs(lm) - 1;
-            lm &= lm - 1;
-            uint32_t jL = __shfl_sync(HC_FULL, j, L);
-            const uint32_t iL = __shfl_sync(HC_FULL, i, L);
-            const uint32_t zL = __shfl_sync(HC_FULL, z, L);
-            uint32_t vL = 0;
-            bool broke = false;
-            walk_warp<Q, SH>(p, txt, sF, lane, jL, iL, zL, vL, broke);
-            if (lane == L) {
-                stepped = true;
-                walk = false;
-                v = vL;
-                if (broke) {
-                    j = jL + p.S;                              // l.12 -> l.18
-                } else {
-                    need_v = v == p.hv;                        // l.14-16
-                    j = e + 1;                                 // (i - q) + (m - q + 1)
+        if (long_walks) {
+            // walks that passed kLongWalk link tests and still have >= kLongWalk steps to
+            // go (near-matches, true matches) finish warp-wide, one lane at a time
+            uint32_t lm = __ballot_sync(HC_FULL, active && walk && wsteps >= kLongWalk &&
+                                                     (j - i) >= kLongWalk * Q);
+            while (lm) {
+                const uint32_t L = __ffs(lm) - 1;
+                lm &= lm - 1;
+                uint32_t jL = __shfl_sync(HC_FULL, j, L);
+                const uint32_t iL = __shfl_sync(HC_FULL, i, L);
+                const uint32_t zL = __shfl_sync(HC_FULL, z, L);
+                uint32_t vL = 0;
+                bool broke = false;
+                walk_warp<Q, SH>(p, txt, sF, lane, jL, iL, zL, vL, broke);
+                if (lane == L) {
+                    stepped = true;
+                    walk = false;
+                    v = vL;
+                    if (broke) {
+                        j = jL + p.S;                              // l.12 -> l.18
+                    } else {
+                        need_v = v == p.hv;                        // l.14-16
+                        j = e + 1;                                 // (i - q) + (m - q + 1)
+                    }
+                    if (j >= b) active = false;
                 }
-                if (j >= b) active = false;
             }
         }
         if (active && !stepped) {
-            const uint32_t pos = walk ? j - p.q : j;
-            const uint32_t vv = qhash<Q, SH>(end8<Q>(txt, pos), p.mask);
+            // positions this iteration may hash: j (window end, if not walking) and
+            // j - t q for the walk steps t = 1..U still allowed (j - (t-1) q >= i)
+            const uint32_t ii = walk ? i : j + 2 * Q - p.m;    // l.7
+            const uint32_t R = j >= ii ? (j - ii) / Q + 1 : 0u;
+            uint32_t vv[U + 1], zz[U + 1];
+#pragma unroll
+            for (int t = 0; t <= U; ++t) {
+                const bool need = t == 0 ? !walk : static_cast<uint32_t>(t) <= R;
+                vv[t] = need ? qhash<Q, SH>(end8<Q>(txt, j - t * Q), p.mask) : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t <= U; ++t) {
+                const bool need = t == 0 ? !walk : static_cast<uint32_t>(t) <= R;
+                zz[t] = need ? sF[vv[t]] : 0u;
+            }
             bool complete = false;
             if (!walk) {                                       // l.4-7
                 e = j;
-                v = vv;
-                z = sF[vv];
+                v = vv[0];
+                z = zz[0];
                 if (z == 0) {
                     j += p.S;                                  // l.18 fast path
                 } else {
-                    i = j + 2 * p.q - p.m;                     // l.7 (> 0)
-                    if (j >= i) walk = true;                   // l.8
-                    else complete = true;                      // m < 2q: while-else (R7)
+                    i = ii;
+                    if (j >= i) {                              // l.8
+                        walk = true;
+                        wsteps = 0;
+                    } else {
+                        complete = true;                       // m < 2q: while-else (R7)
+                    }
                 }
-            } else {                                           // l.9-13
-                j -= p.q;
-                v = vv;
-                if (((z >> (v & (kWordBits - 1))) & 1u) == 0) {
-                    walk = false;                              // l.12 break
-                    j += p.S;                                  // l.18
-                } else {
-                    z = sF[v];                                 // l.13
-                    if (j < i) {
-                        walk = false;
-                        complete = true;
+            }
+#pragma unroll
+            for (int t = 1; t <= U; ++t) {                     // l.9-13, in order
+                if (walk) {
+                    j -= Q;
+                    v = vv[t];
+                    ++wsteps;
+                    if (((z >> (v & (kWordBits - 1))) & 1u) == 0) {
+                        walk = false;                          // l.12 break
+                        j += p.S;                              // l.18
+                    } else {
+                        z = zz[t];                             // l.13
+                        if (j < i) {
+                            walk = false;
+                            complete = true;
+                        }
                     }
                 }
             }
@@ -419,6 +470,25 @@ __device__ __forceinline__ void run_survivors(const KParams &p, const T &txt, co
         }
         wo.push(found, e + 1 - p.m, p, lane);                 // l.17
     }
+    return wo.cnt;
+}
+
+template <int Q, int SH, class T>
+__device__ __forceinline__ void run_segments(const KParams &, const T &txt, const FTable &sF,
+                                             const uint8_t *sx, bool active, uint32_t k,
+                                             WarpOut &wo, uint32_t lane) {
+    wo.cnt = run_segments_impl<Q, SH, T>(txt, sF, sx, active, k, wo.buf, wo.cnt, lane);
+}
+
+// Phase B on `cnt` <= 32 queued segments (queue[lane]), one per lane.
+template <int Q, int SH, class T>
+__device__ __forceinline__ void run_survivors(const KParams &p, const T &txt, const FTable &sF,
+                                              const uint8_t *sx, const uint32_t *queue,
+                                              uint32_t cnt, WarpOut &wo, uint32_t lane) {
+    const bool active = lane < cnt;
+    const uint32_t k = active ? queue[lane] : 0u;
+    __syncwarp();
+    run_segments<Q, SH>(p, txt, sF, sx, active, k, wo, lane);
 }
 
 // Phase A over lattice points [seg_lo, seg_hi), 32 * kUnroll per warp step: every
@@ -487,36 +557,30 @@ struct WarpQueueSink {
     }
 };
 
-// Staged path sink: a CTA-wide queue, so that phase B runs after the tile's filter in
-// full batches of 32 (one partial batch per tile, not one per warp).  If the CTA
-// queue is full the warp runs the overflow itself.
+// Staged path sink: each filter warp appends its survivors to its own region of the
+// stage's queue (ballot ranks, no atomics); the survivor warp later runs them in
+// batches of 32 taken across all regions.  A full region is run by its warp first.
 template <int Q, int SH, class T>
-struct CtaQueueSink {
+struct RegionSink {
     const KParams &p;
     const T &txt;
     const FTable &sF;
     const uint8_t *sx;
-    uint32_t *cq;
-    uint32_t *cq_count;
-    uint32_t *wq;
+    uint32_t *region;   // kRegion entries
+    uint32_t cnt;       // warp-uniform
     WarpOut &wo;
     uint32_t lane;
     __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
         const uint32_t nb = __popc(bm);
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(cq_count, nb);
-        base = __shfl_sync(HC_FULL, base, 0);
-        const uint32_t r = __popc(bm & lanemask_lt());
-        if (base + nb <= kCtaQueue) {
-            if (pass) cq[base + r] = k;
-        } else {
-            const bool local = pass && base + r >= kCtaQueue;
-            if (pass && !local) cq[base + r] = k;
-            const uint32_t lm = __ballot_sync(HC_FULL, local);
-            if (local) wq[__popc(lm & lanemask_lt())] = k;
+        if (cnt + nb > kRegion) {
             __syncwarp();
-            run_survivors<Q, SH>(p, txt, sF, sx, wq, __popc(lm), wo, lane);
+            for (uint32_t b = 0; b < cnt; b += 32)
+                run_survivors<Q, SH>(p, txt, sF, sx, region + b, min(32u, cnt - b), wo, lane);
+            __syncwarp();
+            cnt = 0;
         }
+        if (pass) region[cnt + __popc(bm & lanemask_lt())] = k;
+        cnt += nb;
     }
 };
 
@@ -532,22 +596,27 @@ __device__ __forceinline__ void drain(const KParams &p, const T &txt, const FTab
 }
 
 // ------------------------------------------------------------------ shared layout
+// Staged CTA: NF = NW - kSurvWarps filter warps + kSurvWarps survivor warps.
+// Shared memory: F | x | per-warp queue | per-warp out buffer | survivor regions
+// [stages][NF][kRegion] | region counts [stages][NF] | full[stages] + filtered[stages]
+// mbarriers | stage ring.
 struct StagedLayout {
-    uint32_t f_off, x_off, q_off, wbuf_off, cq_off, cnt_off, mbar_off, stage_off, total;
+    uint32_t f_off, x_off, q_off, wbuf_off, sq_off, cnt_off, full_off, filt_off, stage_off, total;
 };
 __host__ __device__ inline uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m,
                                                       uint32_t stage_bytes, uint32_t stages,
-                                                      uint32_t nwarps) {
+                                                      uint32_t nwarps, uint32_t, uint32_t) {
     StagedLayout L;
     L.f_off = 0;
     L.x_off = round_up((1u << alpha) * 4u, 16);
     L.q_off = L.x_off + round_up(m + 8, 16);
     L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
-    L.cq_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
-    L.cnt_off = L.cq_off + kCtaQueue * 4u;
-    L.mbar_off = L.cnt_off + 16u;
-    L.stage_off = round_up(L.mbar_off + stages * 8u, 128);
+    L.sq_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    L.cnt_off = L.sq_off + stages * nwarps * kRegion * 4u;
+    L.full_off = round_up(L.cnt_off + stages * nwarps * 4u, 8);
+    L.filt_off = L.full_off + stages * 8u;
+    L.stage_off = round_up(L.filt_off + stages * 8u, 128);
     L.total = L.stage_off + stages * stage_bytes;
     return L;
 }
@@ -565,8 +634,10 @@ __host__ __device__ inline GatherLayout gather_layout(uint32_t alpha, uint32_t m
     return L;
 }
 
-int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages) {
-    return static_cast<int>(staged_layout(alpha, m, stage_bytes, stages, kStagedThreads / 32).total);
+int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
+                      uint32_t slot_bytes, uint32_t nbox) {
+    return static_cast<int>(
+        staged_layout(alpha, m, stage_bytes, stages, kStagedThreads / 32, slot_bytes, nbox).total);
 }
 int gather_smem_bytes(uint32_t alpha, uint32_t m) {
     return static_cast<int>(gather_layout(alpha, m, kGatherThreads / 32).total);
@@ -625,92 +696,156 @@ __device__ __forceinline__ void issue_tile(const KParams &p, uint32_t t, uint8_t
     }
 }
 
+// Loads tile t into `stage` (one warp): bytes outside the 16-aligned interior the bulk
+// copy can move (only at the two ends of an unaligned text, or tiny texts) are
+// stored by the lanes first; then lane 0 arms `bar` and issues the bulk copy.  The
+// lanes' stores are ordered before the arrive (syncwarp + release of the arrive).
+__device__ __forceinline__ void load_tile_warp(const KParams &p, uint32_t t, uint8_t *stage,
+                                               uint64_t *bar, uint32_t lane) {
+    if (t == 0 || t + 2 >= p.ntiles) {
+        const TileGeom g = tile_geom(p, t);
+        const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
+        const uintptr_t ga = y + g.lo, gh = y + g.hi;
+        if (g.B <= g.A) {
+            for (uintptr_t a = ga + lane; a < gh; a += 32)
+                stage[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+        } else {
+            for (uintptr_t a = ga + lane; a < g.A; a += 32)
+                stage[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+            for (uintptr_t a = g.B + lane; a < gh; a += 32)
+                stage[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        fence_proxy_async();
+        issue_tile(p, t, stage, bar);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ uint32_t ld_volatile_shared(const uint32_t *a) {
+    return *reinterpret_cast<const volatile uint32_t *>(a);
+}
+__device__ __forceinline__ void st_volatile_shared(uint32_t *a, uint32_t v) {
+    *reinterpret_cast<volatile uint32_t *>(a) = v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(a));
+    return r;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// Warp-specialised staged kernel.  Per stage s of the ring:
+//   full[s]     armed by the producer (expect_tx), completed by the TMA bulk copy;
+//   filtered[s] one arrival per filter warp once its slice of the tile is filtered
+//               and its survivors are in its region of the stage;
+// the survivor warp owning the tile waits filtered[s], runs phase B on the stage's
+// regions (batches of 32 across regions) and refills stage s with the tile `stages`
+// iterations ahead.  Filter warps never wait for survivor work, only for data.
 template <int Q, int SH>
-__global__ void __launch_bounds__(kStagedThreads) staged_kernel(const KParams p) {
+__global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kStagedThreads / 32;
-    const StagedLayout L = staged_layout(p.alpha, p.m, p.stage_bytes, p.stages, NW);
+    constexpr uint32_t NF = NW - kSurvWarps;
+    const StagedLayout L = staged_layout(p.alpha, p.m, p.stage_bytes, p.stages, NW, 0, 0);
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + L.mbar_off);
+    uint32_t *sq = reinterpret_cast<uint32_t *>(smem + L.sq_off);
+    uint32_t *qcnt = reinterpret_cast<uint32_t *>(smem + L.cnt_off);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.full_off);
+    uint64_t *filt = reinterpret_cast<uint64_t *>(smem + L.filt_off);
     uint8_t *stages = smem + L.stage_off;
-    uint32_t *cq = reinterpret_cast<uint32_t *>(smem + L.cq_off);
-    uint32_t *cq_count = reinterpret_cast<uint32_t *>(smem + L.cnt_off);  // [2], by tile parity
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     load_table(p, sFp, sx);
     if (tid == 0) {
-        for (uint32_t st = 0; st < p.stages; ++st) mbar_init(&mbar[st], 1);
+        s_params = p;
+        for (uint32_t st = 0; st < p.stages; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&filt[st], NF);
+        }
         fence_mbar_init();
-        cq_count[0] = cq_count[1] = 0;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == NF) {                                   // prologue: fill the ring
         for (uint32_t st = 0; st < p.stages; ++st) {
             const uint32_t t = blockIdx.x + st * gridDim.x;
-            if (t < p.ntiles) issue_tile(p, t, stages + st * p.stage_bytes, &mbar[st]);
+            if (t < p.ntiles) load_tile_warp(p, t, stages + st * p.stage_bytes, &full[st], lane);
         }
     }
     const FTable sF{smem_u32(sFp)};
-    uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
-    const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
-    const uint32_t y32 = static_cast<uint32_t>(y);
+    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
     const uint32_t stage0 = smem_u32(stages);
 
     uint32_t st = 0, par = 0;
     for (uint32_t it = 0;; ++it) {
         const uint32_t t = blockIdx.x + it * gridDim.x;
         if (t >= p.ntiles) break;
-        uint8_t *sbuf = stages + st * p.stage_bytes;
         const uint32_t k0 = t * p.seg_per_tile;
         const uint32_t k1 = min(k0 + p.seg_per_tile, p.K);
-        const uint32_t lo = k0 * p.S;                       // first text byte of the tile
-        mbar_wait(&mbar[st], par);
-        // tiles at the two text ends may hold bytes outside the 16-aligned interior the
-        // bulk copy moved (unaligned y, tiny texts): plain byte loads for those
-        if (t == 0 || t + 2 >= p.ntiles) {
-            const TileGeom g = tile_geom(p, t);
-            const uintptr_t ga = y + g.lo, gh = y + g.hi;
-            const bool edges = (g.B <= g.A) || (g.A > ga) || (g.B < gh);
-            if (edges) {
-                if (g.B <= g.A) {
-                    for (uintptr_t a = ga + tid; a < gh; a += blockDim.x)
-                        sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
-                } else {
-                    for (uintptr_t a = ga + tid; a < g.A; a += blockDim.x)
-                        sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
-                    for (uintptr_t a = g.B + tid; a < gh; a += blockDim.x)
-                        sbuf[a - g.gbase] = __ldg(reinterpret_cast<const uint8_t *>(a));
+        const uint32_t lo = k0 * p.S;                   // first text byte of the tile
+        uint32_t *q = sq + st * (NF * kRegion);         // NF regions of kRegion entries
+        uint32_t *qc = qcnt + st * NF;                  // entries used per region
+        if (warp < NF) {
+            mbar_wait(&full[st], par);
+            if (warp == 0 && lane == 0) trace_event(p, it, 0);
+            // shared address of text byte p: stage + ((y + lo) & 15) + (p - lo)
+            const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
+            RegionSink<Q, SH, SmemText> sink{p, txt, sF, sx, q + warp * kRegion, 0u, wo, lane};
+            if (p.debug != 1) {
+                const uint32_t nseg = k1 - k0;
+                const uint32_t seg_lo = k0 + (warp * nseg) / NF;
+                const uint32_t seg_hi = k0 + ((warp + 1) * nseg) / NF;
+                filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
+            }
+            __syncwarp();
+            if (warp == 0 && lane == 0) trace_event(p, it, 1);
+            if (lane == 0) {
+                qc[warp] = sink.cnt;
+                mbar_arrive(&filt[st]);                 // release: region + count visible
+            }
+        } else if (it % kSurvWarps == warp - NF) {
+            mbar_wait(&filt[st], par);
+            const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
+            // inclusive prefix of the region counts (lanes < NF), total in every lane
+            uint32_t incl = lane < NF ? qc[lane] : 0u;
+#pragma unroll
+            for (uint32_t o = 1; o < NF; o <<= 1) {
+                const uint32_t t2 = __shfl_up_sync(HC_FULL, incl, o);
+                if (lane >= o) incl += t2;
+            }
+            const uint32_t total = p.debug == 3 ? 0u : __shfl_sync(HC_FULL, incl, NF - 1);
+            if (lane == 0) trace_event(p, it, 3);
+            for (uint32_t b = 0; b < total; b += 32) {
+                // entry g = b + lane lives in region r with excl(r) <= g < incl(r)
+                const uint32_t g = b + lane;
+                uint32_t r = 0, base = 0;
+#pragma unroll
+                for (uint32_t w = 0; w < NF; ++w) {
+                    const uint32_t iw = __shfl_sync(HC_FULL, incl, w);
+                    if (g >= iw) {
+                        r = w + 1;
+                        base = iw;
+                    }
                 }
+                const bool act = g < total;
+                const uint32_t k = act ? q[r * kRegion + (g - base)] : 0u;
+                run_segments<Q, SH>(p, txt, sF, sx, act, k, wo, lane);
             }
-            __syncthreads();
-        }
-        // shared address of text byte p: stage + ((y + lo) & 15) + (p - lo)
-        const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
-        const uint32_t nseg = k1 - k0;
-        const uint32_t seg_lo = k0 + (warp * nseg) / NW;
-        const uint32_t seg_hi = k0 + ((warp + 1) * nseg) / NW;
-        uint32_t *cnt = cq_count + (it & 1u);
-        if (p.debug == 0) {
-            CtaQueueSink<Q, SH, SmemText> sink{p, txt, sF, sx, cq, cnt, queue, wo, lane};
-            filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
-        }
-        __syncthreads();
-        // phase B in full batches of 32 spread over the warps; the other parity's
-        // counter (last read in the previous tile) is reset for the next tile
-        const uint32_t total = min(*cnt, kCtaQueue);
-        if (tid == 0) cq_count[(it & 1u) ^ 1u] = 0;
-        const uint32_t nbatch = (total + 31) / 32;
-        for (uint32_t bt = (warp + it) % NW; bt < nbatch; bt += NW)
-            run_survivors<Q, SH>(p, txt, sF, sx, cq + 32 * bt, min(32u, total - 32 * bt), wo, lane);
-        __syncthreads();  // every warp is done with this stage and with cq
-        if (tid == 0) {
+            __syncwarp();
+            if (lane == 0) trace_event(p, it, 2);
             const uint32_t tn = t + p.stages * gridDim.x;
-            if (tn < p.ntiles) {
-                fence_proxy_async();
-                issue_tile(p, tn, sbuf, &mbar[st]);
-            }
+            if (tn < p.ntiles)
+                load_tile_warp(p, tn, stages + st * p.stage_bytes, &full[st], lane);
         }
         if (++st == p.stages) {
             st = 0;
@@ -729,6 +864,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     uint8_t *sx = smem + L.x_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     load_table(p, sFp, sx);
+    if (tid == 0) s_params = p;
     __syncthreads();
     const FTable sF{fence_value(smem_u32(sFp))};
     uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
@@ -845,7 +981,7 @@ cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int c
                           LaunchInfo *li) {
     KernFn kern = pick<PickStaged>(p.q, p.s);
     if (!kern) return cudaErrorInvalidValue;
-    const int smem = staged_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages);
+    const int smem = staged_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
     return launch_common(kern, p, kStagedThreads, smem, static_cast<int>(p.ntiles), max_ctas,
                          ctas_per_sm, st, li);
 }

@@ -1,7 +1,8 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
-for cfgs in "15360 2" "16384 2" "32768 2"; do
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+for cfgs in "24576 3" "16384 4" "28672 3" "20480 4"; do
   set -- $cfgs
-  echo "== tile=$1 stages=$2"
-  python tools/profile_search.py --m 8 16 32 64 --reps 3 --tile $1 --stages $2 2>&1 | grep "rep=2"
+  for d in 3 0; do
+  echo "== tile=$1 stages=$2 debug=$d"
+  python tools/profile_search.py --m 8 16 32 64 128 --reps 3 --tile $1 --stages $2 --path 1 --debug $d 2>&1 | grep "rep=2"
+  done
 done
-python tools/profile_search.py --m 128 256 512 1024 --reps 3 2>&1 | grep "rep=2"

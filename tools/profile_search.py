@@ -16,6 +16,19 @@ from paper_2310_15711_b200 import hc  # noqa: E402
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
 
+def analyze_trace(tr, grid, T, stages):
+    import numpy as np
+    a = tr[:grid * T * 4].view(grid, T, 4).cpu().numpy().astype(np.float64)
+    t0 = a[a > 0].min()
+    a = np.where(a > 0, a - t0, np.nan) / 1e3   # us since first event
+    fs, fe, se, ss = a[..., 0], a[..., 1], a[..., 2], a[..., 3]
+    med = lambda v: float(np.nanmedian(v)) if np.isfinite(v).any() else float("nan")
+    print(f"  trace (median, us): first data {med(fs[:, 0]):.2f}; filter {med(fe - fs):.2f}; "
+          f"filter end -> surv start {med(ss - fe):.2f}; surv {med(se - ss):.2f}; "
+          f"surv end -> refilled data {med(fs[:, stages:] - se[:, :-stages]):.2f}; "
+          f"tile period {med(fs[:, 1:] - fs[:, :-1]):.2f}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
@@ -29,6 +42,8 @@ def main():
     ap.add_argument("--cps", type=int, default=0)
     ap.add_argument("--debug", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--absent", action="store_true", help="random pattern (likely absent)")
+    ap.add_argument("--trace", type=int, default=0, help="trace N tiles per CTA (staged)")
     args = ap.parse_args()
     cfg = I.CONFIGS[args.config]
     y, block = I.config_text(cfg, args.n)
@@ -44,17 +59,26 @@ def main():
     for m in args.m:
         q, a = cfg.qa[m]
         o, x = I.patterns(cfg, y, m, count=1, block=block)[0]
+        if args.absent:
+            import numpy as np
+            x = np.random.default_rng(m).permutation(x)
         h = hc.prepare(x, q, a)
+        tr = torch.zeros(2048 * max(args.trace, 1) * 4, dtype=torch.int64, device="cuda")
         for r in range(args.reps):
             flush_l2()
+            tr.zero_()
             res, st = hc.search(h, yd, stats=True, path=args.path, tile_bytes=args.tile,
                                 stages=args.stages, seg_per_lane=args.spl, time_kernel=1,
                                 ctas_per_sm=args.cps, debug=args.debug,
-                                tma_chunk=args.chunk)
+                                tma_chunk=args.chunk, trace=tr.data_ptr() if args.trace else 0,
+                                trace_tiles=args.trace)
             torch.cuda.synchronize()
             print(f"m={m} q={q} a={a} rep={r} count={len(res)} kernel_us={st['kernel_ms']*1e3:.1f} "
-                  f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}",
+                  f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}"
+                  + (f" phaseB iters={st['dbg'][0]} calls={st['dbg'][1]}" if args.debug == 5 else ""),
                   flush=True)
+            if args.trace and r == args.reps - 1:
+                analyze_trace(tr, st["grid"], args.trace, args.stages or 3)
 
 
 if __name__ == "__main__":
