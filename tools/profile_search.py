@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--absent", action="store_true", help="random pattern (likely absent)")
     ap.add_argument("--trace", type=int, default=0, help="trace N tiles per CTA (staged)")
+    ap.add_argument("--sw", type=int, default=0, help="survivor warps (staged)")
     args = ap.parse_args()
     cfg = I.CONFIGS[args.config]
     y, block = I.config_text(cfg, args.n)
@@ -71,7 +72,7 @@ def main():
                                 stages=args.stages, seg_per_lane=args.spl, time_kernel=1,
                                 ctas_per_sm=args.cps, debug=args.debug,
                                 tma_chunk=args.chunk, trace=tr.data_ptr() if args.trace else 0,
-                                trace_tiles=args.trace)
+                                trace_tiles=args.trace, surv_warps=args.sw)
             torch.cuda.synchronize()
             print(f"m={m} q={q} a={a} rep={r} count={len(res)} kernel_us={st['kernel_ms']*1e3:.1f} "
                   f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}"
