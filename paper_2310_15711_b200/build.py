@@ -18,13 +18,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhc.so")
-# translation units: (source, extra flags, object name); hc_inst.cu once per q-gram
-# length so that the kernel instantiations compile in parallel
-UNITS = [("hc_api.cpp", [], "hc_api.o"), ("hc_launch.cu", [], "hc_launch.o")] + [
-    ("hc_inst.cu", [f"-DHC_Q={q}"], f"hc_inst_q{q}.o") for q in range(1, 9)]
-HEADERS = ["hc_internal.h", "hc_device.cuh"]
+SOURCES = ["hc_api.cpp", "hc_kernels.cu"]
+HEADERS = ["hc_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-OBJDIR = os.path.join(HERE, "build_obj")
 
 
 def nvcc() -> str:
@@ -38,34 +34,19 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f, _, _ in UNITS] + [os.path.join(CSRC, h) for h in HEADERS]
-    deps += [os.path.join(INCLUDE, "hc.h"), __file__]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "hc.h"),
+                                                                 __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    from concurrent.futures import ThreadPoolExecutor
-    os.makedirs(OBJDIR, exist_ok=True)
-    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-              "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC]
-
-    def compile_unit(u):
-        src, flags, obj = u
-        out = os.path.join(OBJDIR, obj)
-        r = subprocess.run(common + flags + ["-c", os.path.join(CSRC, src), "-o", out],
-                           capture_output=True, text=True)
-        if r.returncode != 0 or verbose:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise subprocess.CalledProcessError(r.returncode, src)
-        return out
-
-    with ThreadPoolExecutor(min(len(UNITS), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(compile_unit, UNITS))
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([nvcc(), *ARCH, "-shared", *objs, "-o", tmp])
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+           "-Xptxas", "-v" if verbose else "-O3", "-shared", "-I", INCLUDE, "-I", CSRC,
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB
 

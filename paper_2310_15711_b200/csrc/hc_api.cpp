@@ -277,25 +277,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     const uint32_t S = m - q + 1;
     const uint32_t nn = static_cast<uint32_t>(n);
     const uint32_t windows = nn - m + 1;
-    // Lattice: segments of L <= S window ends (any partition is exact, R11;
-    // L <= S keeps "a rejected first window finishes the segment").  L is a multiple of
-    // Wd and the origin a0 makes (y + a0) = Wd - 1 mod Wd, so each lattice q-gram is one
-    // aligned Wd-byte word.  Window ends [m-1, a0) are the head segment.
-    uint32_t Wd = 1, Lseg = S;
-    if (S >= 8) {
-        Wd = 8;
-        Lseg = S & ~7u;
-    } else if (S >= 4 && q <= 4) {
-        Wd = 4;
-        Lseg = S & ~3u;
-    }
-    if (o.debug == 7 || o.debug == 12 || o.debug == 13) {  // general unaligned lattice (tests; 12: + filter only)
-        Wd = 1;
-        Lseg = S;
-    }
-    const uint64_t yaddr = reinterpret_cast<uintptr_t>(y_dev);
-    const uint32_t a0 = m - 1 + static_cast<uint32_t>((Wd - 1 - ((yaddr + m - 1) % Wd)) % Wd);
-    const uint32_t K = a0 >= nn ? 0u : (nn - a0 + Lseg - 1) / Lseg;
+    const uint32_t K = (windows + S - 1) / S;
 
     hc::KParams p{};
     p.y = y_dev;
@@ -309,9 +291,6 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     p.hv = h->hv;
     p.S = S;
     p.alpha = h->alpha;
-    p.a0 = a0;
-    p.L = Lseg;
-    p.Wd = Wd;
     p.K = K;
     p.debug = static_cast<uint32_t>(o.debug);
     p.tma_chunk = o.tma_chunk > 0 ? (static_cast<uint32_t>(o.tma_chunk) + 15) & ~15u : 0u;
@@ -323,26 +302,18 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     if (path == HC_PATH_STAGED) {
         uint32_t stage = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultStageBytes;
         // at least 32 segments (one per lane of a warp) per tile
-        const uint32_t need = 32 * Lseg + m + 48;
+        const uint32_t need = 32 * S + m + 48;
         if (stage < need) stage = need;
         stage = (stage + 15) & ~15u;
         // >= 2: a tile's stage is held through the next tile's filter (its survivors)
         p.stages = o.stages > 0 ? std::max<uint32_t>(2u, static_cast<uint32_t>(o.stages))
                                 : kDefaultStages;
         p.stage_bytes = stage;
-        // segments whose bytes [a_k0 - m + 1, a_k1) fit with 16 B of misalignment slack at
-        // each end, plus 8 B for the head segment tile 0 also holds:
-        // (k1-k0)*L + m - 1 + 40 <= stage
-        p.seg_per_tile = (stage - 40 - (m - 1)) / Lseg;
-        // tile 0 always exists: it also carries the head segment [m-1, a0)
-        p.ntiles = std::max(1u, (K + p.seg_per_tile - 1) / p.seg_per_tile);
+        // segments whose bytes [k0*S, m-1+k1*S) fit with 16 B of misalignment slack at
+        // each end: (k1-k0)*S + m - 1 + 32 <= stage
+        p.seg_per_tile = (stage - 32 - (m - 1)) / S;
+        p.ntiles = (K + p.seg_per_tile - 1) / p.seg_per_tile;
         const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, 0, 0);
-        // survivor warps: more when the filter passes many segments (small shifts)
-        p.surv_warps = o.surv_warps > 0 ? std::min(4u, static_cast<uint32_t>(o.surv_warps))
-                                        : (S <= 8 ? 4u : 2u);
-        // consecutive uses of a stage must go to the same survivor warp (their waits on
-        // the stage's filtered barrier are by parity): surv_warps divides stages
-        while (p.stages % p.surv_warps) --p.surv_warps;
         if (smem > max_smem_optin(h->device)) {
             if (o.path == HC_PATH_STAGED) return fail(HC_EINVAL);
             path = HC_PATH_GATHER;
@@ -365,15 +336,6 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     uint32_t count = 0;
     float kms = 0.f;
     hc::LaunchInfo li;
-    // the last CTA sorts up to sort_cap positions in the kernel's shared memory
-    const int kernel_smem = path == HC_PATH_STAGED
-                                ? hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, 0, 0)
-                                : hc::gather_smem_bytes(p.alpha, m);
-    // (one position per thread of the last CTA; larger counts use the sort kernels)
-    const uint32_t block = path == HC_PATH_STAGED ? hc::kStagedThreads : hc::kGatherThreads;
-    p.sort_cap = 1;
-    while (p.sort_cap * 2 <= block && p.sort_cap * 2 * 4 <= static_cast<uint32_t>(kernel_smem))
-        p.sort_cap *= 2;
     for (int attempt = 0;; ++attempt) {
         Scratch *sc = nullptr;
         cudaError_t e = get_scratch(h->device, cap, &sc);
@@ -381,11 +343,6 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         p.counter = sc->buf;
         p.out = want_pos ? sc->buf + 4 : nullptr;
         p.cap = static_cast<uint32_t>(cap);
-        p.dst = want_pos ? pos_out : nullptr;
-        p.k_out = k_out;
-        p.host_count = sc->host_count_dev;
-        volatile uint32_t *hcnt = sc->host_count;
-        *hcnt = 0xffffffffu;
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         const bool timed = o.time_kernel && attempt == 0;
         if (timed) {
@@ -393,61 +350,49 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             cudaEventCreate(&ev1);
             cudaEventRecord(ev0, stream);
         }
+        const char *stage = "search kernel launch";
         e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, o.ctas_per_sm, &li)
                                    : hc::launch_gather(p, stream, o.max_ctas, o.ctas_per_sm, &li);
         ++launches;
         if (timed) cudaEventRecord(ev1, stream);
-        // wait for the last CTA to publish the count in mapped memory; poll the stream
-        // now and then so that a failed launch or fault is reported instead of spinning
-        for (uint32_t spin = 0; e == cudaSuccess && *hcnt == 0xffffffffu; ++spin) {
-            if ((spin & 1023u) == 1023u) {
-                const cudaError_t q = cudaStreamQuery(stream);
-                if (q != cudaSuccess && q != cudaErrorNotReady) e = q;
-                else if (q == cudaSuccess && *hcnt == 0xffffffffu) e = cudaErrorUnknown;
-            }
+        if (e == cudaSuccess) {
+            stage = "finish kernel launch";
+            *sc->host_count = 0xffffffffu;
+            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, sc->host_count_dev, stream);
+            ++launches;
+        }
+        if (e == cudaSuccess) {
+            stage = "search/finish execution";
+            e = cudaStreamSynchronize(stream);
+        }
+        if (timed) {
+            if (e == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
+            cudaEventDestroy(ev0);
+            cudaEventDestroy(ev1);
         }
         if (e != cudaSuccess) {
-            if (timed) {
-                cudaEventDestroy(ev0);
-                cudaEventDestroy(ev1);
-            }
-            // the counters may be left non-zero: force a fresh scratch next time
+            // the counter may be left non-zero: force a fresh scratch next time
             cudaFree(sc->buf);
             sc->buf = nullptr;
             sc->cap = 0;
-            return cuda_fail(e, "search kernel");
+            return cuda_fail(e, stage);
         }
-        count = *hcnt;
+        count = *reinterpret_cast<volatile uint32_t *>(sc->host_count);
         if (o.debug == 5 && stats) {
-            cudaStreamSynchronize(stream);
             cudaMemcpy(stats->dbg, sc->buf + 2, 8, cudaMemcpyDeviceToHost);
             cudaMemset(sc->buf + 2, 0, 8);
         }
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all
-            cudaStreamSynchronize(stream);
-            if (timed) {
-                cudaEventDestroy(ev0);
-                cudaEventDestroy(ev1);
-            }
             cap = count;
             ++reruns;
             continue;
         }
-        if (want_pos && count > p.sort_cap) {
+        if (want_pos && count > hc::kSmallSort) {
             const uint32_t k = static_cast<uint32_t>(std::min<size_t>(count, max_out));
             e = hc::sort_large(sc->buf + 4, count, nn, pos_out, k, stream, &launches);
-            if (timed) cudaEventRecord(ev1, stream);   // the call's device work ends here
             if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
             if (e != cudaSuccess) return cuda_fail(e, "sort");
-        }
-        if (timed) {
-            // device time from the search launch to the end of this call's last kernel
-            // (search + fused finish, plus the ordering kernels when they ran; the host's
-            // count read-back gap before them is included)
-            if (cudaEventSynchronize(ev1) == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
-            cudaEventDestroy(ev0);
-            cudaEventDestroy(ev1);
         }
         break;
     }

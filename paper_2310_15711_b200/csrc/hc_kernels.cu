@@ -1,5 +1,4 @@
-#pragma once
-// hc_device.cuh — sm_100a device side of libhc (included by the per-q kernel units): the Hash Chain searching phase
+// hc_kernels.cu — sm_100a device side of libhc: the Hash Chain searching phase
 // (Fig. 5 left) as data-parallel CUDA kernels.
 //
 // Data parallelism (reading R11): the window ends
@@ -33,6 +32,7 @@
 // Matches go to a per-warp shared buffer, flushed 32 at a time with one
 // atomicAdd (ballot/popc ranks); the host orders them afterwards.
 
+#include <cub/device/device_radix_sort.cuh>
 
 #include <cstdio>
 #include <cstdlib>
@@ -43,14 +43,15 @@ namespace hc {
 
 #define HC_FULL 0xffffffffu
 constexpr uint32_t kWordBits = 32;       // w (R2)
-constexpr uint32_t kLongWalk = 4;        // walks past this many links with as many left go warp-wide
+constexpr uint32_t kLongWalk = 12;       // walks with >= this many steps left go warp-wide
 constexpr uint32_t kCoopVerifyMin = 64;  // m above which verification is warp-wide
 constexpr int kUnroll = 4;               // lattice rounds whose loads are issued together
 constexpr int kWalkUnroll = 4;           // walk steps evaluated per phase-B iteration
+constexpr uint32_t kSurvWarps = 2;       // staged: survivor/producer warps per CTA
 
 // Launch parameters, copied to shared memory at kernel start so that the out-of-line
 // phase-B routine can read them without a stack copy.
-static __shared__ KParams s_params;
+__shared__ KParams s_params;
 constexpr uint32_t kRegion = 64;         // staged: survivor entries per filter warp per slot
 
 // ------------------------------------------------------------------ PTX helpers
@@ -78,7 +79,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "HC_WAIT%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
         "@P1 bra HC_DONE%=;\n\t"
         "bra HC_WAIT%=;\n"
         "HC_DONE%=:\n\t}" ::"r"(smem_u32(bar)),
@@ -130,9 +131,6 @@ struct GlobalText {
     __device__ __forceinline__ uint64_t word(uintptr_t aligned) const {
         return __ldg(reinterpret_cast<const unsigned long long *>(aligned));
     }
-    __device__ __forceinline__ uint32_t word32(uintptr_t aligned) const {
-        return __ldg(reinterpret_cast<const unsigned int *>(aligned));
-    }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return __ldg(y + p); }
     static constexpr bool kLoSafe = false;  // the word before may be outside y
 };
@@ -167,32 +165,15 @@ struct SmemText {
     uint32_t base;
     __device__ __forceinline__ uint32_t addr(uint32_t p) const { return base + p; }
     __device__ __forceinline__ uint64_t word(uint32_t aligned) const { return lds64(aligned); }
-    __device__ __forceinline__ uint32_t word32(uint32_t aligned) const { return lds32(aligned); }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return lds8(base + p); }
     static constexpr bool kLoSafe = true;   // stages never start at shared offset 0
 };
 
-// F (2^alpha words) in shared memory, addressed by shared-space address, and a
-// 32-word "fold" of it: bit (v mod 1024) is set iff some F[v'] != 0 with v' = v mod
-// 1024.  fold bit 0 implies F[v] == 0, so testing the fold first and F[v] only when
-// its bit is set is exactly the test F[v] != 0 (Fig. 5 l.6), with conflict-free
-// shared-memory banks for the common (rejecting) case.
+// F (2^alpha words) in shared memory, addressed by shared-space address.
 struct FTable {
     uint32_t base;
-    uint32_t fold;
     __device__ __forceinline__ uint32_t operator[](uint32_t v) const { return lds32(base + 4 * v); }
-    __device__ __forceinline__ bool nonzero(uint32_t v) const {
-        if (fold == 0) return lds32(base + 4 * v) != 0u;   // no fold (debug 13/14)
-        const uint32_t fw = lds32(fold + 4 * ((v >> 5) & 31u));
-        const uint32_t bit = (fw >> (v & 31u)) & 1u;
-        uint32_t fv = 0;                               // predicated load: no branch
-        asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p ld.shared.u32 %0, [%2];\n\t}"
-            : "+r"(fv)
-            : "r"(bit), "r"(base + 4 * v));
-        return fv != 0u;
-    }
 };
-
 
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
 // top Q bytes are meaningful.  Reads just the aligned 8-byte words holding y[p]
@@ -209,16 +190,6 @@ __device__ __forceinline__ uint64_t end8(const T &t, uint32_t p) {
         if (T::kLoSafe || off + 1 < static_cast<uint32_t>(Q)) lo = t.word(ah - 8);
     }
     return shr64(lo, 8 * (off + 1)) | shl64(hi, 56 - 8 * off);
-}
-
-// The q-gram ending at lattice point p (Fig. 5 l.4) as end8 would return it: the
-// lattice is aligned so that it is one aligned WD-byte word (WD = 8 or 4), or the
-// general two-word read when WD = 1.
-template <int Q, int WD, class T>
-__device__ __forceinline__ uint64_t lattice_word(const T &t, uint32_t p) {
-    if constexpr (WD == 8) return t.word(t.addr(p) - 7);
-    else if constexpr (WD == 4) return static_cast<uint64_t>(t.word32(t.addr(p) - 3)) << 32;
-    else return end8<Q>(t, p);
 }
 
 // Eq. 3 / Fig. 3 Hash: v = 0; for i = p downto p-q+1:
@@ -281,82 +252,56 @@ __device__ __noinline__ bool verify(const T &t, const uint8_t *sx, uint32_t star
     return true;
 }
 
-// The same comparison done by the whole warp, 4 x 8 bytes per lane per round.
+// The same comparison done by the whole warp, 8 bytes per lane per step.
 template <class T>
 __device__ __forceinline__ bool verify_warp(const T &t, const uint8_t *sx, uint32_t start,
                                             uint32_t m, uint32_t lane) {
-    for (uint32_t k0 = 0; k0 < m; k0 += 1024) {
+    for (uint32_t k0 = 0; k0 < m; k0 += 256) {
+        const uint32_t k = k0 + 8 * lane;
         bool bad = false;
-#pragma unroll
-        for (uint32_t r = 0; r < 4; ++r) {
-            const uint32_t k = k0 + 256 * r + 8 * lane;
-            if (k + 8 <= m) {
-                bad |= end8<8>(t, start + k + 7) != *reinterpret_cast<const uint64_t *>(sx + k);
-            } else {
-                for (uint32_t kk = k; kk < m; ++kk) bad |= t.byte(start + kk) != sx[kk];
-            }
+        if (k + 8 <= m) {
+            bad = end8<8>(t, start + k + 7) != *reinterpret_cast<const uint64_t *>(sx + k);
+        } else {
+            for (uint32_t kk = k; kk < m; ++kk) bad |= t.byte(start + kk) != sx[kk];
         }
         if (__any_sync(HC_FULL, bad)) return false;
     }
     return true;
 }
 
-// Fig. 5 l.8-13 for one lane's walk, done by the whole warp: lane l evaluates steps
-// t = 4l .. 4l+3 of the next 128 (hash of the q-gram ending at j-(t+1)q, its word
-// F[v_t]); the link test of step t uses the word of step t-1 (previous register, or
-// the previous lane's last one).  The first failing step is the sequential loop's
-// break (l.12).  On return j is the position of the last evaluated step (the
-// failing one if broke) and v its hash.  On global text the window is prefetched
-// into L2 first, so the rounds and the verification that follows hit L2.
+// Fig. 5 l.8-13 for one lane's walk, done by the whole warp: lane t evaluates step t
+// of the next 32 (hash of the q-gram ending at j-(t+1)q, its word F[v_t]); the link
+// test of step t uses the word of step t-1 (shuffled up).  The first failing step is
+// the sequential loop's break (l.12).  On return j is the position of the last
+// evaluated step (the failing one if broke) and v its hash.
 template <int Q, int SH, class T>
 __device__ __forceinline__ void walk_warp(const KParams &p, const T &txt, const FTable &sF,
                                           uint32_t lane, uint32_t &j, uint32_t i, uint32_t z,
                                           uint32_t &v, bool &broke) {
-    constexpr uint32_t PL = 4;                    // steps per lane per round
-    uint32_t R = (j - i) / Q + 1;                 // steps while j >= i
-    if constexpr (!T::kLoSafe) {
-        const uintptr_t lo = (txt.addr(j - R * Q - 7)) & ~static_cast<uintptr_t>(127);
-        const uintptr_t hi = txt.addr(j);
-        for (uintptr_t a = lo + 128 * lane; a <= hi; a += 128 * 32)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    }
+    uint32_t R = (j - i) / p.q + 1;  // steps while j >= i
     broke = false;
     while (true) {
-        const uint32_t steps = min(R, 32u * PL);
-        uint32_t vt[PL], zt[PL];
-#pragma unroll
-        for (uint32_t s = 0; s < PL; ++s) {
-            const uint32_t t = PL * lane + s;
-            vt[s] = t < steps ? qhash<Q, SH>(end8<Q>(txt, j - (t + 1) * Q), p.mask) : 0u;
+        const uint32_t steps = min(R, 32u);
+        const bool valid = lane < steps;
+        uint32_t vt = 0, zt = 0;
+        if (valid) {
+            vt = qhash<Q, SH>(end8<Q>(txt, j - (lane + 1) * p.q), p.mask);
+            zt = sF[vt];
         }
-#pragma unroll
-        for (uint32_t s = 0; s < PL; ++s) zt[s] = PL * lane + s < steps ? sF[vt[s]] : 0u;
-        uint32_t zprev = __shfl_up_sync(HC_FULL, zt[PL - 1], 1);
+        uint32_t zprev = __shfl_up_sync(HC_FULL, zt, 1);
         if (lane == 0) zprev = z;
-        uint32_t first = 0xffffffffu;             // first failing step of this lane
-#pragma unroll
-        for (int s = PL - 1; s >= 0; --s) {
-            const uint32_t zp = s == 0 ? zprev : zt[s - 1];
-            const bool ok = (zp >> (vt[s] & (kWordBits - 1))) & 1u;
-            if (PL * lane + s < steps && !ok) first = PL * lane + s;
-        }
-        const uint32_t tmin = __reduce_min_sync(HC_FULL, first);
-        const uint32_t tv = tmin != 0xffffffffu ? tmin : steps - 1;   // step whose hash is v
-        uint32_t vsel = vt[0], zsel = zt[0];
-#pragma unroll
-        for (uint32_t s = 1; s < PL; ++s)
-            if ((tv & (PL - 1)) == s) {
-                vsel = vt[s];
-                zsel = zt[s];
-            }
-        v = __shfl_sync(HC_FULL, vsel, tv / PL);
-        if (tmin != 0xffffffffu) {
-            j -= (tmin + 1) * Q;
+        const bool ok = (zprev >> (vt & (kWordBits - 1))) & 1u;
+        const uint32_t fm = __ballot_sync(HC_FULL, valid && !ok);
+        if (fm) {
+            const uint32_t t = __ffs(fm) - 1;
+            j -= (t + 1) * p.q;
+            v = __shfl_sync(HC_FULL, vt, t);
             broke = true;
             return;
         }
-        z = __shfl_sync(HC_FULL, zsel, tv / PL);
-        j -= steps * Q;
+        j -= steps * p.q;
+        z = __shfl_sync(HC_FULL, zt, steps - 1);
+        v = __shfl_sync(HC_FULL, vt, steps - 1);
         R -= steps;
         if (R == 0) return;
     }
@@ -409,15 +354,15 @@ struct WarpOut {
 // loop's; one iteration costs one shared/global round trip instead of one per step.
 template <int Q, int SH, class T>
 __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF, const uint8_t *sx,
-                                                   bool active, uint32_t j0, uint32_t b0,
-                                                   uint32_t *wbuf, uint32_t wcnt, uint32_t lane) {
+                                                   bool active, uint32_t k, uint32_t *wbuf,
+                                                   uint32_t wcnt, uint32_t lane) {
     // One out-of-line copy per kernel: phase B is cold relative to the filter loop and
     // inlining it at every call site multiplied the kernel's code size (I-cache misses).
     const KParams &p = s_params;
     WarpOut wo{wbuf, wcnt};
     constexpr int U = kWalkUnroll;
-    uint32_t j = j0;                           // first window end of the segment
-    const uint32_t b = b0;                     // segment bound (exclusive)
+    uint32_t j = p.m - 1 + k * p.S;            // lattice window end a_k
+    const uint32_t b = min(j + p.S, p.n);      // segment bound
     uint32_t e = 0, i = 0, z = 0, v = 0, wsteps = 0;
     bool walk = false;
     const bool long_walks = p.m >= 2 * kLongWalk * Q;   // warp-wide walks can pay off
@@ -528,24 +473,11 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF,
     return wo.cnt;
 }
 
-// Phase B on lattice segment k of each active lane: window ends [a_k, min(a_k + L, n)).
 template <int Q, int SH, class T>
-__device__ __forceinline__ void run_segments(const KParams &p, const T &txt, const FTable &sF,
+__device__ __forceinline__ void run_segments(const KParams &, const T &txt, const FTable &sF,
                                              const uint8_t *sx, bool active, uint32_t k,
                                              WarpOut &wo, uint32_t lane) {
-    const uint32_t j0 = p.a0 + k * p.L;
-    wo.cnt = run_segments_impl<Q, SH, T>(txt, sF, sx, active, j0, min(j0 + p.L, p.n), wo.buf,
-                                         wo.cnt, lane);
-}
-
-// The head segment [m-1, min(a0, n)) (lane 0 of the calling warp), read from global memory.
-template <int Q, int SH>
-__device__ __forceinline__ void run_head(const KParams &p, const FTable &sF, const uint8_t *sx,
-                                         WarpOut &wo, uint32_t lane) {
-    const uint32_t b0 = min(p.a0, p.n);
-    if (p.m - 1 >= b0) return;
-    wo.cnt = run_segments_impl<Q, SH, GlobalText>(GlobalText{p.y}, sF, sx, lane == 0, p.m - 1, b0,
-                                                  wo.buf, wo.cnt, lane);
+    wo.cnt = run_segments_impl<Q, SH, T>(txt, sF, sx, active, k, wo.buf, wo.cnt, lane);
 }
 
 // Phase B on `cnt` <= 32 queued segments (queue[lane]), one per lane.
@@ -560,36 +492,40 @@ __device__ __forceinline__ void run_survivors(const KParams &p, const T &txt, co
 }
 
 // Phase A over lattice points [seg_lo, seg_hi), 32 * kUnroll per warp step: every
-// lane hashes the q-gram ending at its lattice point a_k = a0 + k L (Fig. 5 l.4)
+// lane hashes the q-gram ending at its lattice point a_k = m-1 + k S (Fig. 5 l.4)
 // and tests F[v] != 0 (l.6).  Survivor segments are handed to `sink` (warp-uniform
 // call, ballot mask + the lane's k).  Full steps run without bounds checks.
-template <int Q, int SH, int WD, class T, class Sink>
-__device__ __forceinline__ void filter_lattice_wd(const KParams &p, const T &txt, const FTable &sF,
-                                                  uint32_t seg_lo, uint32_t seg_hi, uint32_t lane,
-                                                  Sink &sink) {
-    const uint32_t step = 32 * p.L;
-    for (uint32_t k0 = seg_lo; k0 < seg_hi; k0 += 32 * kUnroll) {
-        const uint32_t pos = p.a0 + (k0 + lane) * p.L;  // window end of lattice point k0+lane
+template <int Q, int SH, class T, class Sink>
+__device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, const FTable &sF,
+                                               uint32_t seg_lo, uint32_t seg_hi, uint32_t lane,
+                                               Sink &&sink) {
+    const uint32_t step = 32 * p.S;
+    uint32_t pos = p.m - 1 + (seg_lo + lane) * p.S;   // window end of lattice point seg_lo+lane
+    uint32_t k0 = seg_lo;
+    for (; k0 + 32 * kUnroll <= seg_hi; k0 += 32 * kUnroll, pos += kUnroll * step) {
         uint64_t W[kUnroll];
-        if (k0 + 32 * kUnroll <= seg_hi) {             // full step: no bounds checks
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) W[u] = lattice_word<Q, WD>(txt, pos + u * step);
-        } else {
+        for (int u = 0; u < kUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
+        bool pass[kUnroll];
+        bool any = false;
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
-                W[u] = k0 + u * 32 + lane < seg_hi ? lattice_word<Q, WD>(txt, pos + u * step) : 0ull;
+        for (int u = 0; u < kUnroll; ++u) {
+            pass[u] = sF[qhash<Q, SH>(W[u], p.mask)] != 0u;
+            any |= pass[u];
         }
-        uint32_t passm = 0;                             // bit u: this lane's point u passed
+        if (__any_sync(HC_FULL, any)) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-            if (k0 + u * 32 + lane < seg_hi && sF.nonzero(qhash<Q, SH>(W[u], p.mask))) passm |= 1u << u;
-        if (__any_sync(HC_FULL, passm != 0)) {
-            for (int u = 0; u < kUnroll; ++u) {         // one sink call site (code size)
-                const bool pass = (passm >> u) & 1u;
-                const uint32_t bm = __ballot_sync(HC_FULL, pass);
-                if (bm && !sink(bm, pass, k0 + u * 32 + lane, k0 + u * 32)) return;
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
+                if (bm) sink(bm, pass[u], k0 + u * 32 + lane);
             }
         }
+    }
+    for (; k0 < seg_hi; k0 += 32, pos += step) {       // ragged tail, one round at a time
+        const bool in = k0 + lane < seg_hi;
+        const bool pass = in && sF[qhash<Q, SH>(end8<Q>(txt, pos), p.mask)] != 0u;
+        const uint32_t bm = __ballot_sync(HC_FULL, pass);
+        if (bm) sink(bm, pass, k0 + lane);
     }
 }
 
@@ -605,7 +541,7 @@ struct WarpQueueSink {
     uint32_t &qcnt;
     WarpOut &wo;
     uint32_t lane;
-    __device__ __forceinline__ bool operator()(uint32_t bm, bool pass, uint32_t k, uint32_t) {
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
         if (pass) queue[qcnt + __popc(bm & lanemask_lt())] = k;
         qcnt += __popc(bm);
         if (qcnt >= 32) {
@@ -618,7 +554,6 @@ struct WarpQueueSink {
             __syncwarp();
             qcnt = rest;
         }
-        return true;
     }
 };
 
@@ -627,21 +562,25 @@ struct WarpQueueSink {
 // batches of 32 taken across all regions.  A full region is run by its warp first.
 template <int Q, int SH, class T>
 struct RegionSink {
+    const KParams &p;
+    const T &txt;
+    const FTable &sF;
+    const uint8_t *sx;
     uint32_t *region;   // kRegion entries
     uint32_t cnt;       // warp-uniform
-    uint32_t over;      // first lattice point not recorded (region full), or kNone
-    static constexpr uint32_t kNone = 0xffffffffu;
-    // returns false when the region is full: the caller stops filtering, the survivor
-    // warp then treats every lattice point from `over` to the slice end as a survivor
-    __device__ __forceinline__ bool operator()(uint32_t bm, bool pass, uint32_t k, uint32_t kbase) {
+    WarpOut &wo;
+    uint32_t lane;
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
         const uint32_t nb = __popc(bm);
         if (cnt + nb > kRegion) {
-            over = kbase;
-            return false;
+            __syncwarp();
+            for (uint32_t b = 0; b < cnt; b += 32)
+                run_survivors<Q, SH>(p, txt, sF, sx, region + b, min(32u, cnt - b), wo, lane);
+            __syncwarp();
+            cnt = 0;
         }
         if (pass) region[cnt + __popc(bm & lanemask_lt())] = k;
         cnt += nb;
-        return true;
     }
 };
 
@@ -656,60 +595,8 @@ __device__ __forceinline__ void drain(const KParams &p, const T &txt, const FTab
     }
 }
 
-// Kernel epilogue, every thread of every CTA (after the warp buffers are flushed).
-// The last CTA to finish (exit ticket) publishes the result: when 1 <= count <=
-// sort_cap it orders the positions in shared memory (bitonic sort of distinct keys,
-// the search's shared memory is free by then) and writes the first k_out as int64;
-// then it resets the counters for the next call and writes the count to the host's
-// mapped word (after a system fence, so positions are visible first).
-__device__ __forceinline__ void finish_last_cta(const KParams &p, uint8_t *smem) {
-    __shared__ uint32_t is_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        is_last = atomicAdd(p.counter + 1, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    const uint32_t count = *reinterpret_cast<volatile uint32_t *>(p.counter);
-    if (p.dst && p.k_out && count && count <= p.cap && count <= p.sort_cap) {
-        uint32_t *s = reinterpret_cast<uint32_t *>(smem);
-        const uint32_t k = min(count, p.k_out);
-        uint32_t P = 1;
-        while (P < count) P <<= 1;
-        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x)
-            s[i] = i < count ? __ldcg(p.out + i) : 0xffffffffu;
-        __syncthreads();
-        for (uint32_t size = 2; size <= P; size <<= 1) {
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                    const uint32_t pr = i ^ stride;
-                    if (pr > i) {
-                        const bool asc = (i & size) == 0;
-                        const uint32_t a = s[i], b = s[pr];
-                        if ((a > b) == asc) {
-                            s[i] = b;
-                            s[pr] = a;
-                        }
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) p.dst[i] = static_cast<int64_t>(s[i]);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        p.counter[0] = 0;
-        p.counter[1] = 0;
-        __threadfence_system();
-        *reinterpret_cast<volatile uint32_t *>(p.host_count) = count;
-    }
-}
-
 // ------------------------------------------------------------------ shared layout
-// Staged CTA: NF = NW - NS filter warps + NS = p.surv_warps survivor warps.
+// Staged CTA: NF = NW - kSurvWarps filter warps + kSurvWarps survivor warps.
 // Shared memory: F | x | per-warp queue | per-warp out buffer | survivor regions
 // [stages][NF][kRegion] | region counts [stages][NF] | full[stages] + filtered[stages]
 // mbarriers | stage ring.
@@ -722,12 +609,12 @@ __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m
                                                       uint32_t nwarps, uint32_t, uint32_t) {
     StagedLayout L;
     L.f_off = 0;
-    L.x_off = round_up((1u << alpha) * 4u, 16) + 128u;   // 128 B fold after F
+    L.x_off = round_up((1u << alpha) * 4u, 16);
     L.q_off = L.x_off + round_up(m + 8, 16);
     L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
     L.sq_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
     L.cnt_off = L.sq_off + stages * nwarps * kRegion * 4u;
-    L.full_off = round_up(L.cnt_off + 2 * stages * nwarps * 4u, 8);   // counts + overflow starts
+    L.full_off = round_up(L.cnt_off + stages * nwarps * 4u, 8);
     L.filt_off = L.full_off + stages * 8u;
     L.stage_off = round_up(L.filt_off + stages * 8u, 128);
     L.total = L.stage_off + stages * stage_bytes;
@@ -740,11 +627,20 @@ __host__ __device__ inline GatherLayout gather_layout(uint32_t alpha, uint32_t m
                                                       uint32_t nwarps) {
     GatherLayout L;
     L.f_off = 0;
-    L.x_off = round_up((1u << alpha) * 4u, 16) + 128u;   // 128 B fold after F
+    L.x_off = round_up((1u << alpha) * 4u, 16);
     L.q_off = L.x_off + round_up(m + 8, 16);
     L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
     L.total = L.wbuf_off + nwarps * kWarpBuf * 4u;
     return L;
+}
+
+int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
+                      uint32_t slot_bytes, uint32_t nbox) {
+    return static_cast<int>(
+        staged_layout(alpha, m, stage_bytes, stages, kStagedThreads / 32, slot_bytes, nbox).total);
+}
+int gather_smem_bytes(uint32_t alpha, uint32_t m) {
+    return static_cast<int>(gather_layout(alpha, m, kGatherThreads / 32).total);
 }
 
 __device__ __forceinline__ void load_table(const KParams &p, uint32_t *sF, uint8_t *sx) {
@@ -759,12 +655,6 @@ __device__ __forceinline__ void load_table(const KParams &p, uint32_t *sF, uint8
     for (uint32_t k = threadIdx.x; k < p.m; k += blockDim.x) sx[k] = __ldg(p.x + k);
     // zero the 8-byte tail so 8-byte compares of x never read uninitialised bytes
     if (threadIdx.x < 8) sx[p.m + threadIdx.x] = 0;
-    // fold of F (see FTable), 32 words just after F
-    uint32_t *fold = sF + ((nF + 3) & ~3u);
-    if (threadIdx.x < 32) fold[threadIdx.x] = 0;
-    __syncthreads();
-    for (uint32_t w = threadIdx.x; w < nF; w += blockDim.x)
-        if (sF[w] != 0u) atomicOr(&fold[(w >> 5) & 31u], 1u << (w & 31u));
 }
 
 // Geometry of staged tile t: segments [k0, k1), text bytes [lo, hi).
@@ -778,10 +668,8 @@ __device__ __forceinline__ TileGeom tile_geom(const KParams &p, uint32_t t) {
     TileGeom g;
     g.k0 = t * p.seg_per_tile;
     g.k1 = min(g.k0 + p.seg_per_tile, p.K);
-    // segments [k0, k1) need bytes [a_k0 - m + 1, min(a_k1, n)); tile 0 also holds the
-    // head segment [m-1, a0), i.e. starts at byte 0
-    g.lo = t == 0 ? 0ull : static_cast<uint64_t>(p.a0) + static_cast<uint64_t>(g.k0) * p.L - (p.m - 1);
-    g.hi = min(static_cast<uint64_t>(p.a0) + static_cast<uint64_t>(g.k1) * p.L,
+    g.lo = static_cast<uint64_t>(g.k0) * p.S;
+    g.hi = min(static_cast<uint64_t>(p.m) - 1 + static_cast<uint64_t>(g.k1) * p.S,
                static_cast<uint64_t>(p.n));
     const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
     const uintptr_t ga = y + g.lo;
@@ -862,12 +750,11 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 // the survivor warp owning the tile waits filtered[s], runs phase B on the stage's
 // regions (batches of 32 across regions) and refills stage s with the tile `stages`
 // iterations ahead.  Filter warps never wait for survivor work, only for data.
-template <int Q, int SH, int WD>
+template <int Q, int SH>
 __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kStagedThreads / 32;
-    const uint32_t NS = p.surv_warps;                  // survivor/producer warps
-    const uint32_t NF = NW - NS;                        // filter warps
+    constexpr uint32_t NF = NW - kSurvWarps;
     const StagedLayout L = staged_layout(p.alpha, p.m, p.stage_bytes, p.stages, NW, 0, 0);
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
@@ -894,7 +781,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
             if (t < p.ntiles) load_tile_warp(p, t, stages + st * p.stage_bytes, &full[st], lane);
         }
     }
-    const FTable sF{smem_u32(sFp), (p.debug == 13 || p.debug == 14) ? 0u : smem_u32(sFp + (((1u << p.alpha) + 3) & ~3u))};
+    const FTable sF{smem_u32(sFp)};
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
     const uint32_t stage0 = smem_u32(stages);
@@ -905,60 +792,44 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
         if (t >= p.ntiles) break;
         const uint32_t k0 = t * p.seg_per_tile;
         const uint32_t k1 = min(k0 + p.seg_per_tile, p.K);
-        const uint32_t lo = t == 0 ? 0u : p.a0 + k0 * p.L - (p.m - 1);  // first byte of the tile
+        const uint32_t lo = k0 * p.S;                   // first text byte of the tile
         uint32_t *q = sq + st * (NF * kRegion);         // NF regions of kRegion entries
         uint32_t *qc = qcnt + st * NF;                  // entries used per region
-        uint32_t *qo = qcnt + (p.stages + st) * NF;     // region overflow start per region
-        // filter warp slices: whole blocks of 32 * kUnroll lattice points
-        const uint32_t chunk = ((k1 - k0 + NF - 1) / NF + 32 * kUnroll - 1) / (32 * kUnroll) * (32 * kUnroll);
         if (warp < NF) {
             mbar_wait(&full[st], par);
             if (warp == 0 && lane == 0) trace_event(p, it, 0);
             // shared address of text byte p: stage + ((y + lo) & 15) + (p - lo)
             const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
-            RegionSink<Q, SH, SmemText> sink{q + warp * kRegion, 0u, RegionSink<Q, SH, SmemText>::kNone};
+            RegionSink<Q, SH, SmemText> sink{p, txt, sF, sx, q + warp * kRegion, 0u, wo, lane};
             if (p.debug != 1) {
-                // contiguous slices of whole 32 * kUnroll blocks (one partial block per tile)
-                const uint32_t lo_k = k0 + warp * chunk;
-                if (lo_k < k1)
-                    filter_lattice_wd<Q, SH, WD>(p, txt, sF, lo_k, min(lo_k + chunk, k1), lane, sink);
+                const uint32_t nseg = k1 - k0;
+                const uint32_t seg_lo = k0 + (warp * nseg) / NF;
+                const uint32_t seg_hi = k0 + ((warp + 1) * nseg) / NF;
+                filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
             }
             __syncwarp();
             if (warp == 0 && lane == 0) trace_event(p, it, 1);
             if (lane == 0) {
                 qc[warp] = sink.cnt;
-                qo[warp] = sink.over;
-                mbar_arrive(&filt[st]);                 // release: region + counts visible
+                mbar_arrive(&filt[st]);                 // release: region + count visible
             }
-        } else if (it % NS == warp - NF) {
+        } else if (it % kSurvWarps == warp - NF) {
             mbar_wait(&filt[st], par);
             const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
-            if (t == 0) {                               // head segment [m-1, min(a0, n))
-                const uint32_t hb = min(p.a0, p.n);
-                if (p.m - 1 < hb)
-                    wo.cnt = run_segments_impl<Q, SH, SmemText>(txt, sF, sx, lane == 0, p.m - 1, hb,
-                                                                wo.buf, wo.cnt, lane);
-            }
-            // items of filter warp w (lanes < NF): its region entries, then every lattice
-            // point from its overflow start to its slice end; inclusive prefix over warps
-            uint32_t items = 0, ov = RegionSink<Q, SH, SmemText>::kNone;
-            if (lane < NF) {
-                ov = qo[lane];
-                const uint32_t shi = min(k0 + (lane + 1) * chunk, k1);
-                items = qc[lane] + (ov != RegionSink<Q, SH, SmemText>::kNone ? shi - ov : 0u);
-            }
-            uint32_t incl = items;
+            // inclusive prefix of the region counts (lanes < NF), total in every lane
+            uint32_t incl = lane < NF ? qc[lane] : 0u;
 #pragma unroll
-            for (uint32_t o = 1; o < NW; o <<= 1) {
+            for (uint32_t o = 1; o < NF; o <<= 1) {
                 const uint32_t t2 = __shfl_up_sync(HC_FULL, incl, o);
                 if (lane >= o) incl += t2;
             }
-            const uint32_t total = (p.debug == 3 || (p.debug >= 12 && p.debug <= 14)) ? 0u : __shfl_sync(HC_FULL, incl, NF - 1);
+            const uint32_t total = p.debug == 3 ? 0u : __shfl_sync(HC_FULL, incl, NF - 1);
             if (lane == 0) trace_event(p, it, 3);
             for (uint32_t b = 0; b < total; b += 32) {
-                // item g = b + lane belongs to warp r with excl(r) <= g < incl(r)
+                // entry g = b + lane lives in region r with excl(r) <= g < incl(r)
                 const uint32_t g = b + lane;
                 uint32_t r = 0, base = 0;
+#pragma unroll
                 for (uint32_t w = 0; w < NF; ++w) {
                     const uint32_t iw = __shfl_sync(HC_FULL, incl, w);
                     if (g >= iw) {
@@ -966,10 +837,8 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
                         base = iw;
                     }
                 }
-                const uint32_t cr = qc[min(r, NF - 1)], orr = qo[min(r, NF - 1)];
                 const bool act = g < total;
-                const uint32_t i = g - base;
-                const uint32_t k = !act ? 0u : (i < cr ? q[r * kRegion + i] : orr + (i - cr));
+                const uint32_t k = act ? q[r * kRegion + (g - base)] : 0u;
                 run_segments<Q, SH>(p, txt, sF, sx, act, k, wo, lane);
             }
             __syncwarp();
@@ -984,10 +853,9 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
         }
     }
     wo.flush(p, lane);
-    finish_last_cta(p, smem);
 }
 
-template <int Q, int SH, int WD>
+template <int Q, int SH>
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kGatherThreads / 32;
@@ -998,22 +866,219 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     load_table(p, sFp, sx);
     if (tid == 0) s_params = p;
     __syncthreads();
-    const FTable sF{fence_value(smem_u32(sFp)), smem_u32(sFp + (((1u << p.alpha) + 3) & ~3u))};
+    const FTable sF{fence_value(smem_u32(sFp))};
     uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
     uint32_t qcnt = 0;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
-    if (blockIdx.x == 0 && warp == 0) run_head<Q, SH>(p, sF, sx, wo, lane);
     const GlobalText txt{p.y};
     WarpQueueSink<Q, SH, GlobalText> sink{p, txt, sF, sx, queue, qcnt, wo, lane};
     const uint32_t total_warps = gridDim.x * NW;
     for (uint32_t c = blockIdx.x * NW + warp; c < p.nchunks; c += total_warps) {
         const uint32_t seg_lo = c * p.seg_per_chunk;
         const uint32_t seg_hi = min(seg_lo + p.seg_per_chunk, p.K);
-        filter_lattice_wd<Q, SH, WD>(p, txt, sF, seg_lo, seg_hi, lane, sink);
+        filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
     }
     drain<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);
     wo.flush(p, lane);
-    finish_last_cta(p, smem);
+}
+
+// ------------------------------------------------------------------ launchers
+using KernFn = void (*)(const KParams);
+
+// (q, s) -> kernel instantiation.  s = floor(alpha/q) <= 15/q; for q = 1 the hash
+// is the byte itself and s plays no role.
+template <template <int, int> class Pick>
+static KernFn pick(uint32_t q, uint32_t s) {
+#define HC_C(Q, SH) \
+    if (q == Q && s == SH) return Pick<Q, SH>::fn();
+    if (q == 1) return Pick<1, 0>::fn();
+    HC_C(2, 0) HC_C(2, 1) HC_C(2, 2) HC_C(2, 3) HC_C(2, 4) HC_C(2, 5) HC_C(2, 6) HC_C(2, 7)
+    HC_C(3, 0) HC_C(3, 1) HC_C(3, 2) HC_C(3, 3) HC_C(3, 4) HC_C(3, 5)
+    HC_C(4, 0) HC_C(4, 1) HC_C(4, 2) HC_C(4, 3)
+    HC_C(5, 0) HC_C(5, 1) HC_C(5, 2) HC_C(5, 3)
+    HC_C(6, 0) HC_C(6, 1) HC_C(6, 2)
+    HC_C(7, 0) HC_C(7, 1) HC_C(7, 2)
+    HC_C(8, 0) HC_C(8, 1)
+#undef HC_C
+    return nullptr;
+}
+template <int Q, int SH>
+struct PickStaged {
+    static KernFn fn() { return staged_kernel<Q, SH>; }
+};
+template <int Q, int SH>
+struct PickGather {
+    static KernFn fn() { return gather_kernel<Q, SH>; }
+};
+
+struct KernCache {
+    KernFn fn;
+    int smem;
+    int occ;
+};
+
+static cudaError_t launch_common(KernFn kern, const KParams &p, int threads, int smem,
+                                 int work_units, int max_ctas, int ctas_per_sm, cudaStream_t st,
+                                 LaunchInfo *li) {
+    // per-thread caches of the driver queries (they cost more than a whole large-m
+    // search): the dynamic shared-memory limit is raised once per kernel to the
+    // device maximum (so any later smem size is allowed), occupancy per (kernel, smem)
+    static thread_local KernFn attr_set[128];
+    static thread_local int nattr = 0;
+    static thread_local KernCache cache[256];
+    static thread_local int ncache = 0;
+    static thread_local int sms = 0, smem_max = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    bool have_attr = false;
+    for (int c = 0; c < nattr; ++c) have_attr |= attr_set[c] == kern;
+    if (!have_attr) {
+        cudaFuncAttributes fa;
+        cudaError_t err = cudaFuncGetAttributes(&fa, kern);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_max - static_cast<int>(fa.sharedSizeBytes));
+        if (err != cudaSuccess) {
+            if (std::getenv("HC_DEBUG"))
+                std::fprintf(stderr, "libhc: cudaFuncSetAttribute: %s\n", cudaGetErrorName(err));
+            return err;
+        }
+        if (nattr < 128) attr_set[nattr++] = kern;
+    }
+    if (smem > smem_max) return cudaErrorInvalidValue;
+    int occ = -1;
+    for (int c = 0; c < ncache; ++c)
+        if (cache[c].fn == kern && cache[c].smem == smem) occ = cache[c].occ;
+    if (occ < 0) {
+        cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (err != cudaSuccess) {
+            if (std::getenv("HC_DEBUG"))
+                std::fprintf(stderr, "libhc: occupancy(smem=%d): %s\n", smem, cudaGetErrorName(err));
+            return err;
+        }
+        if (ncache < 256) cache[ncache++] = KernCache{kern, smem, occ};
+    }
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (ctas_per_sm > 0 && occ > ctas_per_sm) occ = ctas_per_sm;
+    long grid = static_cast<long>(sms) * occ;
+    if (grid > work_units) grid = work_units;
+    if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+    if (grid < 1) grid = 1;
+    kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(p);
+    if (li) {
+        li->grid = static_cast<int>(grid);
+        li->block = threads;
+        li->smem = smem;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li) {
+    KernFn kern = pick<PickStaged>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
+    const int smem = staged_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
+    return launch_common(kern, p, kStagedThreads, smem, static_cast<int>(p.ntiles), max_ctas,
+                         ctas_per_sm, st, li);
+}
+
+cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li) {
+    KernFn kern = pick<PickGather>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
+    const int smem = gather_smem_bytes(p.alpha, p.m);
+    const int warps_needed = static_cast<int>(p.nchunks);
+    const int ctas = (warps_needed + kGatherThreads / 32 - 1) / (kGatherThreads / 32);
+    return launch_common(kern, p, kGatherThreads, smem, ctas, max_ctas, ctas_per_sm, st, li);
+}
+
+// ------------------------------------------------------------------ ordering
+__global__ void widen_kernel(const uint32_t *src, int64_t *dst, uint32_t k) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+        dst[i] = static_cast<int64_t>(src[i]);
+}
+
+
+// Runs right after the search kernel, one CTA: publishes the count to the host
+// (mapped pinned word), resets the device counter for the next call, and when
+// 1 <= count <= kSmallSort orders the positions in shared memory (bitonic sort of
+// distinct keys) and writes the first min(count, max_out) as int64.
+__global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const uint32_t *pos,
+                                                      uint32_t cap, int64_t *dst,
+                                                      uint32_t max_out,
+                                                      volatile uint32_t *host_count) {
+    __shared__ uint32_t s[kSmallSort];
+    const uint32_t count = *counter;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *host_count = count;
+        *counter = 0;
+    }
+    if (dst == nullptr || max_out == 0 || count == 0 || count > cap || count > kSmallSort) return;
+    const uint32_t k = min(count, max_out);
+    if (count == 1) {
+        if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(pos[0]);
+        return;
+    }
+    uint32_t P = 1;
+    while (P < count) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < count ? pos[i] : 0xffffffffu;
+    __syncthreads();
+    for (uint32_t size = 2; size <= P; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                const uint32_t pr = i ^ stride;
+                if (pr > i) {
+                    const bool asc = (i & size) == 0;
+                    const uint32_t a = s[i], b = s[pr];
+                    if ((a > b) == asc) {
+                        s[i] = b;
+                        s[pr] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) dst[i] = static_cast<int64_t>(s[i]);
+}
+
+cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
+                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st) {
+    finish_kernel<<<1, 1024, 0, st>>>(counter, pos, cap, dst, max_out, host_count_dev);
+    return cudaGetLastError();
+}
+
+// count > kSmallSort: CUB radix sort on ceil(log2 n) bits, then widen the first k.
+cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
+                       uint32_t k, cudaStream_t st, int *launches) {
+    int end_bit = 1;
+    while (end_bit < 32 && (static_cast<uint64_t>(1) << end_bit) <= n_bound) ++end_bit;
+    uint32_t *alt = nullptr;
+    size_t tmp_bytes = 0;
+    cudaError_t err = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, pos, alt,
+                                                     static_cast<int>(count), 0, end_bit, st);
+    if (err != cudaSuccess) return err;
+    err = cudaMallocAsync(reinterpret_cast<void **>(&alt),
+                          static_cast<size_t>(count) * 4 + tmp_bytes + 256, st);
+    if (err != cudaSuccess) return err;
+    void *tmp = reinterpret_cast<void *>(
+        (reinterpret_cast<uintptr_t>(alt) + static_cast<size_t>(count) * 4 + 255) &
+        ~static_cast<uintptr_t>(255));
+    err = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, pos, alt, static_cast<int>(count), 0,
+                                         end_bit, st);
+    if (err == cudaSuccess) {
+        const uint32_t blocks = min((k + 255) / 256, 148u * 8u);
+        widen_kernel<<<blocks, 256, 0, st>>>(alt, dst, k);
+        err = cudaGetLastError();
+        if (launches) *launches += 1 + (end_bit + 7) / 8 + 1;  // histogram + onesweep passes + widen
+    }
+    cudaError_t e2 = cudaFreeAsync(alt, st);
+    return err != cudaSuccess ? err : e2;
 }
 
 }  // namespace hc
