@@ -98,7 +98,7 @@ typedef struct hc_search_opts {
     int stages;       /* staged: TMA pipeline depth (0 = default) */
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
-    int time_kernel;  /* 1: record CUDA events around the search kernel (stats->kernel_ms) */
+    int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms) */
     int ctas_per_sm;  /* cap on resident CTAs per SM for the persistent grid (0 = occupancy max) */
     int debug;        /* 0; 1 = staged path streams the tiles but skips the search (measures
                          the TMA pipeline alone; results are NOT valid) */
@@ -117,7 +117,8 @@ typedef struct hc_search_stats {
     int64_t tiles;     /* staged: text tiles; gather: lane chunks */
     int launches;      /* kernels launched by this call (search, re-run, sort, copy) */
     int reruns;        /* search re-runs after the position scratch overflowed */
-    float kernel_ms;   /* search kernel time (first launch), if time_kernel */
+    float kernel_ms;   /* if time_kernel: device time from the search launch to the end of the
+                          call's last kernel (search + result ordering), first attempt */
     uint32_t dbg[2];   /* debug == 5: phase-B loop iterations and phase-B calls */
 } hc_search_stats;
 

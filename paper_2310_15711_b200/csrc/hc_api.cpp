@@ -354,23 +354,24 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, o.ctas_per_sm, &li)
                                    : hc::launch_gather(p, stream, o.max_ctas, o.ctas_per_sm, &li);
         ++launches;
-        if (timed) cudaEventRecord(ev1, stream);
         if (e == cudaSuccess) {
             stage = "finish kernel launch";
             *sc->host_count = 0xffffffffu;
             e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, sc->host_count_dev, stream);
             ++launches;
         }
+        // device time of the call: search + finish (count publication, ordering of up to
+        // kSmallSort positions); a CUB ordering below extends it
+        if (timed) cudaEventRecord(ev1, stream);
         if (e == cudaSuccess) {
             stage = "search/finish execution";
             e = cudaStreamSynchronize(stream);
         }
-        if (timed) {
-            if (e == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
-            cudaEventDestroy(ev0);
-            cudaEventDestroy(ev1);
-        }
         if (e != cudaSuccess) {
+            if (timed) {
+                cudaEventDestroy(ev0);
+                cudaEventDestroy(ev1);
+            }
             // the counter may be left non-zero: force a fresh scratch next time
             cudaFree(sc->buf);
             sc->buf = nullptr;
@@ -384,6 +385,10 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         }
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all
+            if (timed) {
+                cudaEventDestroy(ev0);
+                cudaEventDestroy(ev1);
+            }
             cap = count;
             ++reruns;
             continue;
@@ -391,8 +396,14 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         if (want_pos && count > hc::kSmallSort) {
             const uint32_t k = static_cast<uint32_t>(std::min<size_t>(count, max_out));
             e = hc::sort_large(sc->buf + 4, count, nn, pos_out, k, stream, &launches);
+            if (timed) cudaEventRecord(ev1, stream);   // includes the count read-back gap
             if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
             if (e != cudaSuccess) return cuda_fail(e, "sort");
+        }
+        if (timed) {
+            if (cudaEventSynchronize(ev1) == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
+            cudaEventDestroy(ev0);
+            cudaEventDestroy(ev1);
         }
         break;
     }
