@@ -43,7 +43,7 @@ namespace hc {
 
 #define HC_FULL 0xffffffffu
 constexpr uint32_t kWordBits = 32;       // w (R2)
-constexpr uint32_t kLongWalk = 12;       // walks with >= this many steps left go warp-wide
+constexpr uint32_t kLongWalk = 4;        // walks past this many links with as many left go warp-wide
 constexpr uint32_t kCoopVerifyMin = 64;  // m above which verification is warp-wide
 constexpr int kUnroll = 4;               // lattice rounds whose loads are issued together
 constexpr int kWalkUnroll = 4;           // walk steps evaluated per phase-B iteration
@@ -252,56 +252,82 @@ __device__ __noinline__ bool verify(const T &t, const uint8_t *sx, uint32_t star
     return true;
 }
 
-// The same comparison done by the whole warp, 8 bytes per lane per step.
+// The same comparison done by the whole warp, 4 x 8 bytes per lane per round.
 template <class T>
 __device__ __forceinline__ bool verify_warp(const T &t, const uint8_t *sx, uint32_t start,
                                             uint32_t m, uint32_t lane) {
-    for (uint32_t k0 = 0; k0 < m; k0 += 256) {
-        const uint32_t k = k0 + 8 * lane;
+    for (uint32_t k0 = 0; k0 < m; k0 += 1024) {
         bool bad = false;
-        if (k + 8 <= m) {
-            bad = end8<8>(t, start + k + 7) != *reinterpret_cast<const uint64_t *>(sx + k);
-        } else {
-            for (uint32_t kk = k; kk < m; ++kk) bad |= t.byte(start + kk) != sx[kk];
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) {
+            const uint32_t k = k0 + 256 * r + 8 * lane;
+            if (k + 8 <= m) {
+                bad |= end8<8>(t, start + k + 7) != *reinterpret_cast<const uint64_t *>(sx + k);
+            } else {
+                for (uint32_t kk = k; kk < m; ++kk) bad |= t.byte(start + kk) != sx[kk];
+            }
         }
         if (__any_sync(HC_FULL, bad)) return false;
     }
     return true;
 }
 
-// Fig. 5 l.8-13 for one lane's walk, done by the whole warp: lane t evaluates step t
-// of the next 32 (hash of the q-gram ending at j-(t+1)q, its word F[v_t]); the link
-// test of step t uses the word of step t-1 (shuffled up).  The first failing step is
-// the sequential loop's break (l.12).  On return j is the position of the last
-// evaluated step (the failing one if broke) and v its hash.
+// Fig. 5 l.8-13 for one lane's walk, done by the whole warp: lane l evaluates steps
+// t = 4l .. 4l+3 of the next 128 (hash of the q-gram ending at j-(t+1)q, its word
+// F[v_t]); the link test of step t uses the word of step t-1 (previous register, or
+// the previous lane's last one).  The first failing step is the sequential loop's
+// break (l.12).  On return j is the position of the last evaluated step (the
+// failing one if broke) and v its hash.  On global text the window is prefetched
+// into L2 first, so the rounds and the verification that follows hit L2.
 template <int Q, int SH, class T>
 __device__ __forceinline__ void walk_warp(const KParams &p, const T &txt, const FTable &sF,
                                           uint32_t lane, uint32_t &j, uint32_t i, uint32_t z,
                                           uint32_t &v, bool &broke) {
-    uint32_t R = (j - i) / p.q + 1;  // steps while j >= i
+    constexpr uint32_t PL = 4;                    // steps per lane per round
+    uint32_t R = (j - i) / Q + 1;                 // steps while j >= i
+    if constexpr (!T::kLoSafe) {
+        const uintptr_t lo = (txt.addr(j - R * Q - 7)) & ~static_cast<uintptr_t>(127);
+        const uintptr_t hi = txt.addr(j);
+        for (uintptr_t a = lo + 128 * lane; a <= hi; a += 128 * 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
     broke = false;
     while (true) {
-        const uint32_t steps = min(R, 32u);
-        const bool valid = lane < steps;
-        uint32_t vt = 0, zt = 0;
-        if (valid) {
-            vt = qhash<Q, SH>(end8<Q>(txt, j - (lane + 1) * p.q), p.mask);
-            zt = sF[vt];
+        const uint32_t steps = min(R, 32u * PL);
+        uint32_t vt[PL], zt[PL];
+#pragma unroll
+        for (uint32_t s = 0; s < PL; ++s) {
+            const uint32_t t = PL * lane + s;
+            vt[s] = t < steps ? qhash<Q, SH>(end8<Q>(txt, j - (t + 1) * Q), p.mask) : 0u;
         }
-        uint32_t zprev = __shfl_up_sync(HC_FULL, zt, 1);
+#pragma unroll
+        for (uint32_t s = 0; s < PL; ++s) zt[s] = PL * lane + s < steps ? sF[vt[s]] : 0u;
+        uint32_t zprev = __shfl_up_sync(HC_FULL, zt[PL - 1], 1);
         if (lane == 0) zprev = z;
-        const bool ok = (zprev >> (vt & (kWordBits - 1))) & 1u;
-        const uint32_t fm = __ballot_sync(HC_FULL, valid && !ok);
-        if (fm) {
-            const uint32_t t = __ffs(fm) - 1;
-            j -= (t + 1) * p.q;
-            v = __shfl_sync(HC_FULL, vt, t);
+        uint32_t first = 0xffffffffu;             // first failing step of this lane
+#pragma unroll
+        for (int s = PL - 1; s >= 0; --s) {
+            const uint32_t zp = s == 0 ? zprev : zt[s - 1];
+            const bool ok = (zp >> (vt[s] & (kWordBits - 1))) & 1u;
+            if (PL * lane + s < steps && !ok) first = PL * lane + s;
+        }
+        const uint32_t tmin = __reduce_min_sync(HC_FULL, first);
+        const uint32_t tv = tmin != 0xffffffffu ? tmin : steps - 1;   // step whose hash is v
+        uint32_t vsel = vt[0], zsel = zt[0];
+#pragma unroll
+        for (uint32_t s = 1; s < PL; ++s)
+            if ((tv & (PL - 1)) == s) {
+                vsel = vt[s];
+                zsel = zt[s];
+            }
+        v = __shfl_sync(HC_FULL, vsel, tv / PL);
+        if (tmin != 0xffffffffu) {
+            j -= (tmin + 1) * Q;
             broke = true;
             return;
         }
-        j -= steps * p.q;
-        z = __shfl_sync(HC_FULL, zt, steps - 1);
-        v = __shfl_sync(HC_FULL, vt, steps - 1);
+        z = __shfl_sync(HC_FULL, zsel, tv / PL);
+        j -= steps * Q;
         R -= steps;
         if (R == 0) return;
     }
