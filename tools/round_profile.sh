@@ -1,0 +1,14 @@
+#!/bin/bash
+# bench + ncu evidence for profiles/ (run on the GPU box)
+set -x
+timeout 300 python -m pytest tests/test_gpu_parity.py -q 2>&1 | tail -1 > gpurun_out/parity.txt
+timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+# launch list of one bench step (reduced: 5 patterns per m) -- cold-cache, serialised
+python bench.py --steps 1 --warmup 3 --per-m 5 --no-e2e --no-cpu > gpurun_out/bench_small.json 2> gpurun_out/bench_small.err && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 1 --warmup 3 --per-m 5 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
+# full capture of the dominant kernel (staged, m=16) and the gather kernel (m=512)
+python tools/profile_search.py --m 16 512 --reps 1 > gpurun_out/pf_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"staged|gather" -c 2 \
+    -o gpurun_out/prof_round python tools/profile_search.py --m 16 512 --reps 1 > gpurun_out/ncu_full.log 2>&1
+echo done
