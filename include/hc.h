@@ -101,7 +101,9 @@ typedef struct hc_search_opts {
     int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms) */
     int ctas_per_sm;  /* cap on resident CTAs per SM for the persistent grid (0 = occupancy max) */
     int debug;        /* 0; 1 = staged path streams the tiles but skips the search (measures
-                         the TMA pipeline alone; results are NOT valid) */
+                         the TMA pipeline alone; 3 = phase A only; 6 = phase A on stale
+                         stage data without waiting for TMA (filter compute alone); results
+                         are NOT valid for debug != 0) */
     int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage) */
     unsigned long long *trace; /* staged, debugging: DEVICE buffer of grid x trace_tiles x 4
                                   %globaltimer stamps per (CTA, tile), or NULL */

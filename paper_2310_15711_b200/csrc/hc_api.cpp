@@ -164,6 +164,9 @@ int max_smem_optin(int dev) {
 constexpr uint32_t kStagedMaxShift = 96;
 constexpr uint32_t kDefaultStageBytes = 24576;
 constexpr uint32_t kDefaultStages = 2;
+// dynamic shared memory per staged CTA for 3 CTAs per SM: 228 KB per SM, 1 KB
+// reserved per CTA, 1.3 KB static
+constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
 constexpr uint32_t kDefaultSegPerLane = 4;
 
 }  // namespace
@@ -305,15 +308,25 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         const uint32_t need = 32 * S + m + 48;
         if (stage < need) stage = need;
         stage = (stage + 15) & ~15u;
-        // >= 2: a tile's stage is held through the next tile's filter (its survivors)
-        p.stages = o.stages > 0 ? std::max<uint32_t>(2u, static_cast<uint32_t>(o.stages))
+        // an even number (2..16): each of the 2 survivor warps owns every other
+        // iteration, hence the tile chains of half the stages
+        p.stages = o.stages > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.stages) + 1u) & ~1u
                                 : kDefaultStages;
         p.stage_bytes = stage;
         // segments whose bytes [k0*S, m-1+k1*S) fit with 16 B of misalignment slack at
         // each end: (k1-k0)*S + m - 1 + 32 <= stage
         p.seg_per_tile = (stage - 32 - (m - 1)) / S;
         p.ntiles = (K + p.seg_per_tile - 1) / p.seg_per_tile;
-        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, 0, 0);
+        // survivor boxes of the survivor warps: a segment's text (<= m + S - 1 bytes)
+        // in whole 16-byte chunks, as many as fit next to the stages for 3 CTAs per SM
+        p.slot_bytes = 16 * ((m + S + 29) / 16);
+        {
+            const uint32_t fixed = static_cast<uint32_t>(
+                hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, 0)) + 16;
+            const uint32_t room = fixed < kStagedSmem3 ? kStagedSmem3 - fixed : 0u;
+            p.nbox = std::min<uint32_t>(64u, room / (2 * (p.slot_bytes + 8)));
+        }
+        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
         if (smem > max_smem_optin(h->device)) {
             if (o.path == HC_PATH_STAGED) return fail(HC_EINVAL);
             path = HC_PATH_GATHER;
@@ -354,6 +367,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, o.ctas_per_sm, &li)
                                    : hc::launch_gather(p, stream, o.max_ctas, o.ctas_per_sm, &li);
         ++launches;
+        if (timed && o.debug == 7) cudaEventRecord(ev1, stream);   // search kernel alone
         if (e == cudaSuccess) {
             stage = "finish kernel launch";
             *sc->host_count = 0xffffffffu;
@@ -362,7 +376,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         }
         // device time of the call: search + finish (count publication, ordering of up to
         // kSmallSort positions); a CUB ordering below extends it
-        if (timed) cudaEventRecord(ev1, stream);
+        if (timed && o.debug != 7) cudaEventRecord(ev1, stream);
         if (e == cudaSuccess) {
             stage = "search/finish execution";
             e = cudaStreamSynchronize(stream);

@@ -52,7 +52,7 @@ constexpr uint32_t kSurvWarps = 2;       // staged: survivor/producer warps per 
 // Launch parameters, copied to shared memory at kernel start so that the out-of-line
 // phase-B routine can read them without a stack copy.
 __shared__ KParams s_params;
-constexpr uint32_t kRegion = 64;         // staged: survivor entries per filter warp per slot
+constexpr uint32_t kRegion = 32;         // staged: survivor entries per filter warp per slot
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -79,7 +79,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "HC_WAIT%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@P1 bra HC_DONE%=;\n\t"
         "bra HC_WAIT%=;\n"
         "HC_DONE%=:\n\t}" ::"r"(smem_u32(bar)),
@@ -95,6 +95,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Programmatic dependent launch: the search kernels let the finish kernel launch
+// early (its CTA then waits in griddepcontrol.wait for the search grid to complete
+// and its memory to be visible), hiding the finish kernel's launch latency.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -103,6 +110,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void trace_event(const KParams &p, uint32_t it, uint32_t ev) {
     if (p.trace && it < p.trace_tiles)
         p.trace[(static_cast<size_t>(blockIdx.x) * p.trace_tiles + it) * 4 + ev] = gtimer();
+}
+// CTA entry (ev 0) / exit (ev 1) stamps after the per-tile records (one thread)
+__device__ __forceinline__ void trace_cta(const KParams &p, uint32_t ev) {
+    if (p.trace)
+        p.trace[static_cast<size_t>(gridDim.x) * p.trace_tiles * 4 + blockIdx.x * 2 + ev] = gtimer();
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
@@ -132,6 +144,7 @@ struct GlobalText {
         return __ldg(reinterpret_cast<const unsigned long long *>(aligned));
     }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return __ldg(y + p); }
+    __device__ __forceinline__ GlobalText shfl(uint32_t) const { return *this; }  // same in all lanes
     static constexpr bool kLoSafe = false;  // the word before may be outside y
 };
 
@@ -166,7 +179,11 @@ struct SmemText {
     __device__ __forceinline__ uint32_t addr(uint32_t p) const { return base + p; }
     __device__ __forceinline__ uint64_t word(uint32_t aligned) const { return lds64(aligned); }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return lds8(base + p); }
-    static constexpr bool kLoSafe = true;   // stages never start at shared offset 0
+    // lane L's mapping (survivor boxes: every lane has its own)
+    __device__ __forceinline__ SmemText shfl(uint32_t L) const {
+        return SmemText{__shfl_sync(0xffffffffu, base, L)};
+    }
+    static constexpr bool kLoSafe = true;   // stages/boxes never start at shared offset 0
 };
 
 // F (2^alpha words) in shared memory, addressed by shared-space address.
@@ -372,7 +389,8 @@ struct WarpOut {
     }
 };
 
-// Phase B: HC (Fig. 5) on one segment per active lane (lattice point k), warp-
+// Phase B: HC (Fig. 5) on one segment per active lane, from the window end `start`
+// inside the segment (the lattice point a_k, or where first_steps left it), warp-
 // synchronous.  Each iteration a lane evaluates its window-end hash (l.4-6) and up to
 // kWalkUnroll walk steps (l.9-13): the hashes and F words of all positions it may
 // need (j, j-q, ..., never below the window) are loaded in parallel, then the link
@@ -380,15 +398,16 @@ struct WarpOut {
 // loop's; one iteration costs one shared/global round trip instead of one per step.
 template <int Q, int SH, class T>
 __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF, const uint8_t *sx,
-                                                   bool active, uint32_t k, uint32_t *wbuf,
+                                                   bool active, uint32_t start, uint32_t *wbuf,
                                                    uint32_t wcnt, uint32_t lane) {
     // One out-of-line copy per kernel: phase B is cold relative to the filter loop and
     // inlining it at every call site multiplied the kernel's code size (I-cache misses).
     const KParams &p = s_params;
     WarpOut wo{wbuf, wcnt};
     constexpr int U = kWalkUnroll;
-    uint32_t j = p.m - 1 + k * p.S;            // lattice window end a_k
-    const uint32_t b = min(j + p.S, p.n);      // segment bound
+    uint32_t j = start;                        // a window end inside segment k
+    const uint32_t k = (start - (p.m - 1)) / p.S;
+    const uint32_t b = min(p.m - 1 + (k + 1) * p.S, p.n);   // segment bound
     uint32_t e = 0, i = 0, z = 0, v = 0, wsteps = 0;
     bool walk = false;
     const bool long_walks = p.m >= 2 * kLongWalk * Q;   // warp-wide walks can pay off
@@ -409,7 +428,7 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF,
                 const uint32_t zL = __shfl_sync(HC_FULL, z, L);
                 uint32_t vL = 0;
                 bool broke = false;
-                walk_warp<Q, SH>(p, txt, sF, lane, jL, iL, zL, vL, broke);
+                walk_warp<Q, SH>(p, txt.shfl(L), sF, lane, jL, iL, zL, vL, broke);
                 if (lane == L) {
                     stepped = true;
                     walk = false;
@@ -488,7 +507,7 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF,
                 const uint32_t L = __ffs(vm) - 1;
                 vm &= vm - 1;
                 const uint32_t st = __shfl_sync(HC_FULL, e + 1 - p.m, L);
-                const bool ok = verify_warp(txt, sx, st, p.m, lane);
+                const bool ok = verify_warp(txt.shfl(L), sx, st, p.m, lane);
                 if (lane == L) found = ok;
             }
         } else if (need_v) {
@@ -501,9 +520,9 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FTable sF,
 
 template <int Q, int SH, class T>
 __device__ __forceinline__ void run_segments(const KParams &, const T &txt, const FTable &sF,
-                                             const uint8_t *sx, bool active, uint32_t k,
+                                             const uint8_t *sx, bool active, uint32_t start,
                                              WarpOut &wo, uint32_t lane) {
-    wo.cnt = run_segments_impl<Q, SH, T>(txt, sF, sx, active, k, wo.buf, wo.cnt, lane);
+    wo.cnt = run_segments_impl<Q, SH, T>(txt, sF, sx, active, start, wo.buf, wo.cnt, lane);
 }
 
 // Phase B on `cnt` <= 32 queued segments (queue[lane]), one per lane.
@@ -568,7 +587,7 @@ struct WarpQueueSink {
     WarpOut &wo;
     uint32_t lane;
     __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
-        if (pass) queue[qcnt + __popc(bm & lanemask_lt())] = k;
+        if (pass) queue[qcnt + __popc(bm & lanemask_lt())] = p.m - 1 + k * p.S;   // a_k
         qcnt += __popc(bm);
         if (qcnt >= 32) {
             __syncwarp();
@@ -583,20 +602,33 @@ struct WarpQueueSink {
     }
 };
 
-// Staged path sink: each filter warp appends its survivors to its own region of the
-// stage's queue (ballot ranks, no atomics); the survivor warp later runs them in
-// batches of 32 taken across all regions.  A full region is run by its warp first.
+// Staged path sink.  Lattice survivors (segment k) are collected per warp (q1) and
+// run 32 at a time through first_steps, a lane-parallel evaluation of the first
+// steps of Fig. 5 for the window e = a_k (F[v_0] != 0 already, l.6) when m >= 2q:
+// the walk's first step (l.9-12) tests the link bit of v_1 = h(y[e-2q+1..e-q]) in
+// F[v_0]; if it is clear the loop breaks and the next window ends at j = e - q + S
+// (l.18); if F[h(j)] == 0 that window shifts by S again (l.6) to
+// j + S >= a_k + S, out of the segment (R11), and the segment is finished.
+// Otherwise the segment continues at e (link set) or at j.  Exact: these are the
+// paper's steps in order, with the three hashes loaded in parallel.  On DNA this
+// finishes ~90% of the lattice survivors at the cost of one shared-memory round
+// trip per 32.  The rest go, as the window end to continue from, to the warp's
+// region of the stage's queue, which the survivor warp runs in batches of 32 taken
+// across all regions (a full region is run by its warp first).
 template <int Q, int SH, class T>
 struct RegionSink {
     const KParams &p;
     const T &txt;
     const FTable &sF;
     const uint8_t *sx;
-    uint32_t *region;   // kRegion entries
+    uint32_t *region;   // kRegion entries (window ends)
     uint32_t cnt;       // warp-uniform
+    uint32_t *q1;       // kWarpBuf lattice survivors (k)
+    uint32_t n1;        // warp-uniform
     WarpOut &wo;
     uint32_t lane;
-    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
+    __device__ __forceinline__ void push(bool keep, uint32_t start) {
+        const uint32_t bm = __ballot_sync(HC_FULL, keep);
         const uint32_t nb = __popc(bm);
         if (cnt + nb > kRegion) {
             __syncwarp();
@@ -605,8 +637,51 @@ struct RegionSink {
             __syncwarp();
             cnt = 0;
         }
-        if (pass) region[cnt + __popc(bm & lanemask_lt())] = k;
+        if (keep) region[cnt + __popc(bm & lanemask_lt())] = start;
         cnt += nb;
+    }
+    __device__ __forceinline__ void first_steps(uint32_t c) {
+        const bool act = lane < c;
+        const uint32_t k = act ? q1[lane] : 0u;
+        const uint32_t e = p.m - 1 + k * p.S;
+        uint32_t start = e;
+        bool keep = act;
+        if (act && p.m >= 2 * Q) {
+            const uint32_t j = e - Q + p.S;
+            const bool jin = j < p.n;                    // else the break leaves the text
+            const uint64_t W0 = end8<Q>(txt, e), W1 = end8<Q>(txt, e - Q);
+            const uint64_t W2 = end8<Q>(txt, jin ? j : e);
+            const uint32_t v1 = qhash<Q, SH>(W1, p.mask);
+            const uint32_t z0 = sF[qhash<Q, SH>(W0, p.mask)];
+            const uint32_t z2 = sF[qhash<Q, SH>(W2, p.mask)];
+            if (((z0 >> (v1 & (kWordBits - 1))) & 1u) == 0u) {   // break at the first step
+                keep = jin && z2 != 0u;
+                start = j;
+            }
+        }
+        push(keep, start);
+    }
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
+        if (p.debug == 3) return;                        // phase A only (measurement)
+        if (pass) q1[n1 + __popc(bm & lanemask_lt())] = k;
+        n1 += __popc(bm);
+        if (n1 >= 32) {
+            __syncwarp();
+            first_steps(32);
+            const uint32_t rest = n1 - 32;
+            const uint32_t mv = lane < rest ? q1[32 + lane] : 0u;
+            __syncwarp();
+            if (lane < rest) q1[lane] = mv;
+            __syncwarp();
+            n1 = rest;
+        }
+    }
+    __device__ __forceinline__ void finish() {           // before the stage is handed on
+        if (n1) {
+            __syncwarp();
+            first_steps(n1);
+            n1 = 0;
+        }
     }
 };
 
@@ -624,15 +699,18 @@ __device__ __forceinline__ void drain(const KParams &p, const T &txt, const FTab
 // ------------------------------------------------------------------ shared layout
 // Staged CTA: NF = NW - kSurvWarps filter warps + kSurvWarps survivor warps.
 // Shared memory: F | x | per-warp queue | per-warp out buffer | survivor regions
-// [stages][NF][kRegion] | region counts [stages][NF] | full[stages] + filtered[stages]
-// mbarriers | stage ring.
+// [stages][NW][kRegion] | region counts [stages][NW] | full[stages] + filtered[stages]
+// mbarriers | tile id per stage | survivor-warp box meta [kSurvWarps][nbox][2] |
+// survivor boxes [kSurvWarps][nbox][slot_bytes] | stage ring.
 struct StagedLayout {
-    uint32_t f_off, x_off, q_off, wbuf_off, sq_off, cnt_off, full_off, filt_off, stage_off, total;
+    uint32_t f_off, x_off, q_off, wbuf_off, sq_off, cnt_off, full_off, filt_off, tile_off, meta_off,
+        box_off, stage_off, total;
 };
 __host__ __device__ inline uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m,
                                                       uint32_t stage_bytes, uint32_t stages,
-                                                      uint32_t nwarps, uint32_t, uint32_t) {
+                                                      uint32_t nwarps, uint32_t slot_bytes,
+                                                      uint32_t nbox) {
     StagedLayout L;
     L.f_off = 0;
     L.x_off = round_up((1u << alpha) * 4u, 16);
@@ -642,7 +720,10 @@ __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m
     L.cnt_off = L.sq_off + stages * nwarps * kRegion * 4u;
     L.full_off = round_up(L.cnt_off + stages * nwarps * 4u, 8);
     L.filt_off = L.full_off + stages * 8u;
-    L.stage_off = round_up(L.filt_off + stages * 8u, 128);
+    L.tile_off = L.filt_off + stages * 8u;
+    L.meta_off = L.tile_off + stages * 4u;
+    L.box_off = round_up(L.meta_off + kSurvWarps * nbox * 8u, 16);
+    L.stage_off = round_up(L.box_off + kSurvWarps * nbox * slot_bytes, 128);
     L.total = L.stage_off + stages * stage_bytes;
     return L;
 }
@@ -771,67 +852,102 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 
 // Warp-specialised staged kernel.  Per stage s of the ring:
 //   full[s]     armed by the producer (expect_tx), completed by the TMA bulk copy;
+//               tile[s] (written before the arm) says which tile, >= ntiles = none;
 //   filtered[s] one arrival per filter warp once its slice of the tile is filtered
-//               and its survivors are in its region of the stage;
-// the survivor warp owning the tile waits filtered[s], runs phase B on the stage's
-// regions (batches of 32 across regions) and refills stage s with the tile `stages`
-// iterations ahead.  Filter warps never wait for survivor work, only for data.
+//               (first_steps included) and its survivors are in its region of s;
+// the survivor warp owning the iteration waits filtered[s], takes the survivors'
+// window ends out of the regions, refills stage s at once with the next tile of a
+// global counter (dynamic scheduling: CTAs that run ahead take more tiles, so the
+// grid finishes together), and then runs phase B on them reading the text from
+// global memory (the tile was just streamed through L2): survivors never hold a
+// stage.  Filter warps never wait for survivor work, only for data.
 template <int Q, int SH>
 __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kStagedThreads / 32;
     constexpr uint32_t NF = NW - kSurvWarps;
-    const StagedLayout L = staged_layout(p.alpha, p.m, p.stage_bytes, p.stages, NW, 0, 0);
+    const StagedLayout L = staged_layout(p.alpha, p.m, p.stage_bytes, p.stages, NW, p.slot_bytes,
+                                         p.nbox);
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
     uint32_t *sq = reinterpret_cast<uint32_t *>(smem + L.sq_off);
     uint32_t *qcnt = reinterpret_cast<uint32_t *>(smem + L.cnt_off);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.full_off);
     uint64_t *filt = reinterpret_cast<uint64_t *>(smem + L.filt_off);
+    volatile uint32_t *tile = reinterpret_cast<volatile uint32_t *>(smem + L.tile_off);
     uint8_t *stages = smem + L.stage_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) trace_cta(p, 0);
+    pdl_launch_dependents();
 
+    // loads tile t (or nothing, t >= ntiles) into stage st: the tile id is published
+    // before the barrier is armed (the arm releases it to the waiters)
+    auto produce = [&](uint32_t st, uint32_t t) {
+        if (lane == 0) tile[st] = t;
+        __syncwarp();
+        if (t < p.ntiles) {
+            load_tile_warp(p, t, stages + st * p.stage_bytes, &full[st], lane);
+        } else if (lane == 0) {
+            mbar_arrive(&full[st]);
+        }
+        __syncwarp();
+    };
+    // the producer warp starts the first tiles' copies before the table load
+    if (warp == NF) {
+        if (lane == 0) {
+            for (uint32_t st = 0; st < p.stages; ++st) {
+                mbar_init(&full[st], 1);
+                mbar_init(&filt[st], NF);
+            }
+            fence_mbar_init();
+        }
+        __syncwarp();
+        for (uint32_t st = 0; st < p.stages; ++st) produce(st, blockIdx.x + st * gridDim.x);
+    }
     load_table(p, sFp, sx);
-    if (tid == 0) {
-        s_params = p;
-        for (uint32_t st = 0; st < p.stages; ++st) {
-            mbar_init(&full[st], 1);
-            mbar_init(&filt[st], NF);
-        }
-        fence_mbar_init();
-    }
+    if (tid == 0) s_params = p;
     __syncthreads();
-    if (warp == NF) {                                   // prologue: fill the ring
-        for (uint32_t st = 0; st < p.stages; ++st) {
-            const uint32_t t = blockIdx.x + st * gridDim.x;
-            if (t < p.ntiles) load_tile_warp(p, t, stages + st * p.stage_bytes, &full[st], lane);
-        }
-    }
     const FTable sF{smem_u32(sFp)};
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
     const uint32_t stage0 = smem_u32(stages);
+    const bool dynamic = p.debug != 6;
 
-    uint32_t st = 0, par = 0;
-    for (uint32_t it = 0;; ++it) {
-        const uint32_t t = blockIdx.x + it * gridDim.x;
-        if (t >= p.ntiles) break;
-        const uint32_t k0 = t * p.seg_per_tile;
-        const uint32_t k1 = min(k0 + p.seg_per_tile, p.K);
-        const uint32_t lo = k0 * p.S;                   // first text byte of the tile
-        uint32_t *q = sq + st * (NF * kRegion);         // NF regions of kRegion entries
-        uint32_t *qc = qcnt + st * NF;                  // entries used per region
-        if (warp < NF) {
-            mbar_wait(&full[st], par);
+    if (warp < NF) {
+        // Each stage carries a chain of tiles (produced in order by the survivor warp
+        // owning the stage's iterations) that ends with the first "no tile"; the filter
+        // warps go round the stages until every chain has ended.
+        const uint32_t all = (1u << p.stages) - 1u;
+        uint32_t ended = 0, st = 0, par = 0;
+        for (uint32_t it = 0; ended != all; ++it) {
+            if (((ended >> st) & 1u) == 0) {
+            // debug 6: filter compute alone (stale stage data, static tiles, no refills)
+            if (dynamic || it < p.stages) mbar_wait(&full[st], par);
+            const uint32_t t = dynamic ? fence_value(tile[st]) : blockIdx.x + it * gridDim.x;
+            uint32_t *q = sq + st * (NF * kRegion);     // NF regions of kRegion entries
+            uint32_t *qc = qcnt + st * NF;              // entries used per region
+            if (t >= p.ntiles) {
+                ended |= 1u << st;
+                if (lane == 0) {
+                    qc[warp] = 0;
+                    mbar_arrive(&filt[st]);             // lets the survivor warp see the end
+                }
+            } else {
             if (warp == 0 && lane == 0) trace_event(p, it, 0);
+            const uint32_t k0 = t * p.seg_per_tile;
+            const uint32_t k1 = min(k0 + p.seg_per_tile, p.K);
+            const uint32_t lo = k0 * p.S;               // first text byte of the tile
             // shared address of text byte p: stage + ((y + lo) & 15) + (p - lo)
-            const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
-            RegionSink<Q, SH, SmemText> sink{p, txt, sF, sx, q + warp * kRegion, 0u, wo, lane};
+            const SmemText txt{stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo};
+            RegionSink<Q, SH, SmemText> sink{p,  txt, sF, sx, q + warp * kRegion, 0u,
+                                             reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf,
+                                             0u, wo, lane};
             if (p.debug != 1) {
                 const uint32_t nseg = k1 - k0;
                 const uint32_t seg_lo = k0 + (warp * nseg) / NF;
                 const uint32_t seg_hi = k0 + ((warp + 1) * nseg) / NF;
                 filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
+                sink.finish();
             }
             __syncwarp();
             if (warp == 0 && lane == 0) trace_event(p, it, 1);
@@ -839,9 +955,27 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
                 qc[warp] = sink.cnt;
                 mbar_arrive(&filt[st]);                 // release: region + count visible
             }
-        } else if (it % kSurvWarps == warp - NF) {
+            }
+            }
+            if (++st == p.stages) {
+                st = 0;
+                par ^= 1u;
+            }
+        }
+    } else if (dynamic) {
+        // survivor warp NF + i owns the iterations it = i, i + kSurvWarps, ...; it
+        // grabs the tile it will produce next one iteration ahead (hides the atomic)
+        uint32_t nt = 0;
+        if (lane == 0) nt = p.stages * gridDim.x + atomicAdd(p.counter + 1, 1u);
+        for (uint32_t it = warp - NF;; it += kSurvWarps) {
+            const uint32_t st = it % p.stages, par = (it / p.stages) & 1u;
             mbar_wait(&filt[st], par);
-            const SmemText txt{fence_value(stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo)};
+            const uint32_t t = fence_value(tile[st]);
+            if (t >= p.ntiles) break;
+            const uint32_t lo = t * p.seg_per_tile * p.S;
+            uint32_t *q = sq + st * (NF * kRegion);
+            const uint32_t *qc = qcnt + st * NF;
+            const SmemText txt{stage0 + st * p.stage_bytes + ((y32 + lo) & 15u) - lo};
             // inclusive prefix of the region counts (lanes < NF), total in every lane
             uint32_t incl = lane < NF ? qc[lane] : 0u;
 #pragma unroll
@@ -851,9 +985,8 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
             }
             const uint32_t total = p.debug == 3 ? 0u : __shfl_sync(HC_FULL, incl, NF - 1);
             if (lane == 0) trace_event(p, it, 3);
-            for (uint32_t b = 0; b < total; b += 32) {
-                // entry g = b + lane lives in region r with excl(r) <= g < incl(r)
-                const uint32_t g = b + lane;
+            // entry g lives in region r with excl(r) <= g < incl(r)
+            auto entry = [&](uint32_t g) -> uint32_t {
                 uint32_t r = 0, base = 0;
 #pragma unroll
                 for (uint32_t w = 0; w < NF; ++w) {
@@ -863,22 +996,57 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
                         base = iw;
                     }
                 }
-                const bool act = g < total;
-                const uint32_t k = act ? q[r * kRegion + (g - base)] : 0u;
-                run_segments<Q, SH>(p, txt, sF, sx, act, k, wo, lane);
+                return g < total ? q[r * kRegion + (g - base)] : 0u;
+            };
+            // The survivors are taken out of the stage before it is refilled: the first
+            // nbox as boxes (their segment's text copied in 16-byte chunks to this
+            // warp's box area, based so that text p is at base + p), the next kWarpBuf
+            // as window ends only (phase B reads them from global memory), the rest
+            // (rare after first_steps) are run on the stage first.
+            uint32_t *meta = reinterpret_cast<uint32_t *>(smem + L.meta_off) + (warp - NF) * 2 * p.nbox;
+            const uint32_t box0 = smem_u32(smem + L.box_off) + (warp - NF) * p.nbox * p.slot_bytes;
+            uint32_t *mine = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
+            const uint32_t nb = min(total, p.nbox);
+            const uint32_t nm = min(total - nb, static_cast<uint32_t>(kWarpBuf));
+            for (uint32_t b = nb + nm; b < total; b += 32) {
+                const uint32_t start = entry(b + lane);
+                run_segments<Q, SH>(p, txt, sF, sx, b + lane < total, start, wo, lane);
+            }
+            for (uint32_t b = 0; b < nb + nm; b += 32) {
+                const uint32_t g = b + lane;
+                const uint32_t start = entry(g);
+                if (g < nb) {
+                    const uint32_t k = (start - (p.m - 1)) / p.S;
+                    const uint32_t hi = min(p.m - 1 + (k + 1) * p.S, p.n);
+                    const uint32_t a0 = (txt.base + start + 1 - p.m) & ~15u;
+                    const uint32_t a1 = (txt.base + hi - 1) & ~15u;
+                    const uint32_t d0 = box0 + g * p.slot_bytes;
+                    for (uint32_t a = a0, d = d0; a <= a1; a += 16, d += 16) sts128(d, lds128(a));
+                    meta[2 * g] = start;
+                    meta[2 * g + 1] = d0 - (a0 - txt.base);
+                } else if (g < nb + nm) {
+                    mine[g - nb] = start;
+                }
+            }
+            __syncwarp();
+            produce(st, __shfl_sync(HC_FULL, nt, 0));
+            if (lane == 0) nt = p.stages * gridDim.x + atomicAdd(p.counter + 1, 1u);
+            for (uint32_t b = 0; b < nb; b += 32) {
+                const bool act = b + lane < nb;
+                const SmemText btxt{act ? meta[2 * (b + lane) + 1] : txt.base};
+                run_segments<Q, SH>(p, btxt, sF, sx, act, act ? meta[2 * (b + lane)] : 0u, wo, lane);
+            }
+            const GlobalText gtxt{p.y};
+            for (uint32_t b = 0; b < nm; b += 32) {
+                const bool act = b + lane < nm;
+                run_segments<Q, SH>(p, gtxt, sF, sx, act, act ? mine[b + lane] : 0u, wo, lane);
             }
             __syncwarp();
             if (lane == 0) trace_event(p, it, 2);
-            const uint32_t tn = t + p.stages * gridDim.x;
-            if (tn < p.ntiles)
-                load_tile_warp(p, tn, stages + st * p.stage_bytes, &full[st], lane);
-        }
-        if (++st == p.stages) {
-            st = 0;
-            par ^= 1u;
         }
     }
     wo.flush(p, lane);
+    if (lane == 0) trace_cta(p, 1);   // last warp to get here wins
 }
 
 template <int Q, int SH>
@@ -889,6 +1057,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    pdl_launch_dependents();
     load_table(p, sFp, sx);
     if (tid == 0) s_params = p;
     __syncthreads();
@@ -1038,11 +1207,13 @@ __global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const u
                                                       uint32_t max_out,
                                                       volatile uint32_t *host_count) {
     __shared__ uint32_t s[kSmallSort];
+    pdl_wait();   // the search grid has completed and its writes are visible
     const uint32_t count = *counter;
     __syncthreads();
     if (threadIdx.x == 0) {
         *host_count = count;
-        *counter = 0;
+        counter[0] = 0;
+        counter[1] = 0;   // staged path: dynamic tile counter
     }
     if (dst == nullptr || max_out == 0 || count == 0 || count > cap || count > kSmallSort) return;
     const uint32_t k = min(count, max_out);
@@ -1075,8 +1246,18 @@ __global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const u
 
 cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
                           uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st) {
-    finish_kernel<<<1, 1024, 0, st>>>(counter, pos, cap, dst, max_out, host_count_dev);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, finish_kernel, counter, pos, cap, dst, max_out,
+                              host_count_dev);
 }
 
 // count > kSmallSort: CUB radix sort on ceil(log2 n) bits, then widen the first k.

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhc.so")
+# HC_LIB: another build of the same library (A/B experiments in tools/)
+LIB_PATH = os.environ.get("HC_LIB") or os.path.join(_HERE, "libhc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2310_15711_b200.build` "

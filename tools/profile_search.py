@@ -27,6 +27,14 @@ def analyze_trace(tr, grid, T, stages):
           f"filter end -> surv start {med(ss - fe):.2f}; surv {med(se - ss):.2f}; "
           f"surv end -> refilled data {med(fs[:, stages:] - se[:, :-stages]):.2f}; "
           f"tile period {med(fs[:, 1:] - fs[:, :-1]):.2f}")
+    ce = tr[grid * T * 4: grid * T * 4 + 2 * grid].view(grid, 2).cpu().numpy().astype(np.float64)
+    ce = (ce - t0) / 1e3
+    print(f"  CTA entry min {ce[:, 0].min():.2f} p50 {np.median(ce[:, 0]):.2f} max {ce[:, 0].max():.2f}; "
+          f"exit p50 {np.median(ce[:, 1]):.2f} max {ce[:, 1].max():.2f} (us vs first tile event)")
+    last = np.nanmax(np.where(np.isfinite(fe), fe, np.nan), axis=1)   # per CTA, last traced filter end
+    print(f"  span: first event 0, CTA last-traced-filter-end p50 {np.nanpercentile(last, 50):.2f} "
+          f"p90 {np.nanpercentile(last, 90):.2f} max {np.nanmax(last):.2f} us; "
+          f"CTA first data p50 {np.nanpercentile(fs[:, 0], 50):.2f} max {np.nanmax(fs[:, 0]):.2f}")
 
 
 def main():
@@ -64,7 +72,7 @@ def main():
             import numpy as np
             x = np.random.default_rng(m).permutation(x)
         h = hc.prepare(x, q, a)
-        tr = torch.zeros(2048 * max(args.trace, 1) * 4, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(2048 * max(args.trace, 1) * 4 + 4096 + 2048 * 32, dtype=torch.int64, device="cuda")
         for r in range(args.reps):
             flush_l2()
             tr.zero_()
@@ -80,6 +88,14 @@ def main():
                   flush=True)
             if args.trace and r == args.reps - 1:
                 analyze_trace(tr, st["grid"], args.trace, args.stages or 3)
+                if args.debug == 11:
+                    import numpy as np
+                    g = st["grid"]
+                    b0 = g * args.trace * 4 + 2 * g
+                    pr = tr[b0:b0 + g * 8 * 4].view(g, 8, 4).cpu().numpy().astype(np.float64) / 1965.0
+                    print("  per-warp us (wait, filter, tail, release): mean",
+                          np.round(pr.mean(axis=(0, 1)), 2), "max-over-warps mean",
+                          np.round(pr.max(axis=1).mean(axis=0), 2))
 
 
 if __name__ == "__main__":
