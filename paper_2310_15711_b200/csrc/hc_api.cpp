@@ -159,15 +159,16 @@ int max_smem_optin(int dev) {
     return v > 0 ? v : 48 * 1024;
 }
 
-// Default path choice: stage the whole text when the shift is
-// small enough that HC touches every 32-B sector anyway; gather otherwise.
-constexpr uint32_t kStagedMaxShift = 96;
+// Default path choice: stage the whole text when the shift is small
+// (the lattice is dense and filtering from shared memory pays); gather otherwise.
+// Measured on C2 (B200): staged ahead up to m = 32 (S = 27), gather from m = 48.
+constexpr uint32_t kStagedMaxShift = 32;
 constexpr uint32_t kDefaultStageBytes = 24576;
 constexpr uint32_t kDefaultStages = 2;
 // dynamic shared memory per staged CTA for 3 CTAs per SM: 228 KB per SM, 1 KB
 // reserved per CTA, 1.3 KB static
 constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
-constexpr uint32_t kDefaultSegPerLane = 4;
+constexpr uint32_t kDefaultSegPerLane = 2;
 
 }  // namespace
 
@@ -334,7 +335,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     }
     if (path == HC_PATH_GATHER) {
         const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)
-                                                : kDefaultSegPerLane;
+                                                : (S >= 512 ? 1u : kDefaultSegPerLane);
         p.seg_per_chunk = 32 * spl;
         p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
         if (hc::gather_smem_bytes(p.alpha, m) > max_smem_optin(h->device)) return fail(HC_EINVAL);

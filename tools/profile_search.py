@@ -66,7 +66,7 @@ def main():
         # dirty lines whose write-back then competes with the timed search)
         flush.view(torch.int64).sum()
     for m in args.m:
-        q, a = cfg.qa[m]
+        q, a = cfg.qa[m] if m in cfg.qa else cfg.qa[min(cfg.qa, key=lambda k: abs(k - m))]
         o, x = I.patterns(cfg, y, m, count=1, block=block)[0]
         if args.absent:
             import numpy as np
