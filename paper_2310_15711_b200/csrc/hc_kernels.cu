@@ -574,47 +574,99 @@ __device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, c
     }
 }
 
-// Gather path sink: per-warp queue, phase B whenever 32 are queued (survivors read
-// global memory, so the queue may span chunks).
+// first_steps: the first steps of Fig. 5 for the window e = a_k of a lattice survivor
+// (F[v_0] != 0 already, l.6), evaluated lane-parallel, when m >= 2q: the walk's first
+// step (l.9-12) tests the link bit of v_1 = h(y[e-2q+1..e-q]) in F[v_0]; if it is
+// clear the loop breaks and the next window ends at j = e - q + S (l.18); if
+// F[h(j)] == 0 that window shifts by S again (l.6) to j + S >= a_k + S, out of
+// the segment (R11), and the segment is finished (returns false).  Otherwise the
+// segment continues at `start` = e (link set) or j.  Exact: these are the paper's
+// steps in order, with the three hashes loaded in parallel.  On DNA this finishes
+// ~90% of the lattice survivors for one memory round trip per 32.
+template <int Q, int SH, class T>
+__device__ __forceinline__ bool first_steps_eval(const KParams &p, const T &txt, const FTable &sF,
+                                                 bool act, uint32_t k, uint32_t &start) {
+    const uint32_t e = p.m - 1 + k * p.S;
+    start = e;
+    if (!act) return false;
+    if (p.m < 2 * Q) return true;                        // no walk step to test (R7)
+    const uint32_t j = e - Q + p.S;
+    const bool jin = j < p.n;                            // else the break leaves the text
+    const uint64_t W0 = end8<Q>(txt, e), W1 = end8<Q>(txt, e - Q);
+    const uint64_t W2 = end8<Q>(txt, jin ? j : e);
+    const uint32_t v1 = qhash<Q, SH>(W1, p.mask);
+    const uint32_t z0 = sF[qhash<Q, SH>(W0, p.mask)];
+    const uint32_t z2 = sF[qhash<Q, SH>(W2, p.mask)];
+    if (((z0 >> (v1 & (kWordBits - 1))) & 1u) != 0u) return true;   // link set: walk on
+    start = j;                                           // break at the first step
+    return jin && z2 != 0u;
+}
+
+// Gather path sink: lattice survivors (k) are queued per warp (q1) and run 32 at a
+// time through first_steps_eval; the segments that continue go to a second queue
+// (q2, window ends) that runs phase B whenever 32 are queued (both queues may span
+// chunks, since the survivors read global memory).
 template <int Q, int SH, class T>
 struct WarpQueueSink {
     const KParams &p;
     const T &txt;
     const FTable &sF;
     const uint8_t *sx;
-    uint32_t *queue;
-    uint32_t &qcnt;
+    uint32_t *q1, *q2;     // kWarpBuf entries each
+    uint32_t n1, n2;       // warp-uniform
     WarpOut &wo;
     uint32_t lane;
+    __device__ __forceinline__ void steps(uint32_t c) {  // first steps of q1[0..c) -> q2
+        const bool act = lane < c;
+        uint32_t start;
+        const bool keep = first_steps_eval<Q, SH>(p, txt, sF, act, act ? q1[lane] : 0u, start);
+        const uint32_t bm = __ballot_sync(HC_FULL, keep);
+        if (keep) q2[n2 + __popc(bm & lanemask_lt())] = start;
+        n2 += __popc(bm);
+        if (n2 >= 32) {
+            __syncwarp();
+            run_survivors<Q, SH>(p, txt, sF, sx, q2, 32, wo, lane);
+            const uint32_t rest = n2 - 32;
+            const uint32_t nv = lane < rest ? q2[32 + lane] : 0u;
+            __syncwarp();
+            if (lane < rest) q2[lane] = nv;
+            __syncwarp();
+            n2 = rest;
+        }
+    }
     __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
-        if (pass) queue[qcnt + __popc(bm & lanemask_lt())] = p.m - 1 + k * p.S;   // a_k
-        qcnt += __popc(bm);
-        if (qcnt >= 32) {
+        if (pass) q1[n1 + __popc(bm & lanemask_lt())] = k;
+        n1 += __popc(bm);
+        if (n1 >= 32) {
             __syncwarp();
-            run_survivors<Q, SH>(p, txt, sF, sx, queue, 32, wo, lane);
-            const uint32_t rest = qcnt - 32;
-            const uint32_t nv = lane < rest ? queue[32 + lane] : 0u;
+            steps(32);
+            const uint32_t rest = n1 - 32;
+            const uint32_t nv = lane < rest ? q1[32 + lane] : 0u;
             __syncwarp();
-            if (lane < rest) queue[lane] = nv;
+            if (lane < rest) q1[lane] = nv;
             __syncwarp();
-            qcnt = rest;
+            n1 = rest;
+        }
+    }
+    __device__ __forceinline__ void drain() {
+        if (n1) {
+            __syncwarp();
+            steps(n1);
+            n1 = 0;
+        }
+        if (n2) {
+            __syncwarp();
+            run_survivors<Q, SH>(p, txt, sF, sx, q2, n2, wo, lane);
+            n2 = 0;
         }
     }
 };
 
 // Staged path sink.  Lattice survivors (segment k) are collected per warp (q1) and
-// run 32 at a time through first_steps, a lane-parallel evaluation of the first
-// steps of Fig. 5 for the window e = a_k (F[v_0] != 0 already, l.6) when m >= 2q:
-// the walk's first step (l.9-12) tests the link bit of v_1 = h(y[e-2q+1..e-q]) in
-// F[v_0]; if it is clear the loop breaks and the next window ends at j = e - q + S
-// (l.18); if F[h(j)] == 0 that window shifts by S again (l.6) to
-// j + S >= a_k + S, out of the segment (R11), and the segment is finished.
-// Otherwise the segment continues at e (link set) or at j.  Exact: these are the
-// paper's steps in order, with the three hashes loaded in parallel.  On DNA this
-// finishes ~90% of the lattice survivors at the cost of one shared-memory round
-// trip per 32.  The rest go, as the window end to continue from, to the warp's
-// region of the stage's queue, which the survivor warp runs in batches of 32 taken
-// across all regions (a full region is run by its warp first).
+// run 32 at a time through first_steps_eval.  The rest go, as the window end to
+// continue from, to the warp's region of the stage's queue, which the survivor warp
+// runs in batches of 32 taken across all regions (a full region is run by its warp
+// first).
 template <int Q, int SH, class T>
 struct RegionSink {
     const KParams &p;
@@ -642,23 +694,8 @@ struct RegionSink {
     }
     __device__ __forceinline__ void first_steps(uint32_t c) {
         const bool act = lane < c;
-        const uint32_t k = act ? q1[lane] : 0u;
-        const uint32_t e = p.m - 1 + k * p.S;
-        uint32_t start = e;
-        bool keep = act;
-        if (act && p.m >= 2 * Q) {
-            const uint32_t j = e - Q + p.S;
-            const bool jin = j < p.n;                    // else the break leaves the text
-            const uint64_t W0 = end8<Q>(txt, e), W1 = end8<Q>(txt, e - Q);
-            const uint64_t W2 = end8<Q>(txt, jin ? j : e);
-            const uint32_t v1 = qhash<Q, SH>(W1, p.mask);
-            const uint32_t z0 = sF[qhash<Q, SH>(W0, p.mask)];
-            const uint32_t z2 = sF[qhash<Q, SH>(W2, p.mask)];
-            if (((z0 >> (v1 & (kWordBits - 1))) & 1u) == 0u) {   // break at the first step
-                keep = jin && z2 != 0u;
-                start = j;
-            }
-        }
+        uint32_t start;
+        const bool keep = first_steps_eval<Q, SH>(p, txt, sF, act, act ? q1[lane] : 0u, start);
         push(keep, start);
     }
     __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
@@ -684,17 +721,6 @@ struct RegionSink {
         }
     }
 };
-
-template <int Q, int SH, class T>
-__device__ __forceinline__ void drain(const KParams &p, const T &txt, const FTable &sF,
-                                      const uint8_t *sx, uint32_t *queue, uint32_t &qcnt,
-                                      WarpOut &wo, uint32_t lane) {
-    if (qcnt) {
-        __syncwarp();
-        run_survivors<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);
-        qcnt = 0;
-    }
-}
 
 // ------------------------------------------------------------------ shared layout
 // Staged CTA: NF = NW - kSurvWarps filter warps + kSurvWarps survivor warps.
@@ -728,7 +754,7 @@ __host__ __device__ inline StagedLayout staged_layout(uint32_t alpha, uint32_t m
     return L;
 }
 struct GatherLayout {
-    uint32_t f_off, x_off, q_off, wbuf_off, total;
+    uint32_t f_off, x_off, q_off, q2_off, wbuf_off, total;
 };
 __host__ __device__ inline GatherLayout gather_layout(uint32_t alpha, uint32_t m,
                                                       uint32_t nwarps) {
@@ -736,7 +762,8 @@ __host__ __device__ inline GatherLayout gather_layout(uint32_t alpha, uint32_t m
     L.f_off = 0;
     L.x_off = round_up((1u << alpha) * 4u, 16);
     L.q_off = L.x_off + round_up(m + 8, 16);
-    L.wbuf_off = L.q_off + nwarps * kWarpBuf * 4u;
+    L.q2_off = L.q_off + nwarps * kWarpBuf * 4u;
+    L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
     L.total = L.wbuf_off + nwarps * kWarpBuf * 4u;
     return L;
 }
@@ -1062,18 +1089,19 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     if (tid == 0) s_params = p;
     __syncthreads();
     const FTable sF{fence_value(smem_u32(sFp))};
-    uint32_t *queue = reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf;
-    uint32_t qcnt = 0;
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const GlobalText txt{p.y};
-    WarpQueueSink<Q, SH, GlobalText> sink{p, txt, sF, sx, queue, qcnt, wo, lane};
+    WarpQueueSink<Q, SH, GlobalText> sink{p, txt, sF, sx,
+                                          reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf,
+                                          reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
+                                          0u, 0u, wo, lane};
     const uint32_t total_warps = gridDim.x * NW;
     for (uint32_t c = blockIdx.x * NW + warp; c < p.nchunks; c += total_warps) {
         const uint32_t seg_lo = c * p.seg_per_chunk;
         const uint32_t seg_hi = min(seg_lo + p.seg_per_chunk, p.K);
         filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
     }
-    drain<Q, SH>(p, txt, sF, sx, queue, qcnt, wo, lane);
+    sink.drain();
     wo.flush(p, lane);
 }
 

@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--absent", action="store_true", help="random pattern (likely absent)")
     ap.add_argument("--trace", type=int, default=0, help="trace N tiles per CTA (staged)")
     ap.add_argument("--sw", type=int, default=0, help="survivor warps (staged)")
+    ap.add_argument("--noflush", action="store_true", help="no L2 flush between calls")
     args = ap.parse_args()
     cfg = I.CONFIGS[args.config]
     y, block = I.config_text(cfg, args.n)
@@ -74,7 +75,8 @@ def main():
         h = hc.prepare(x, q, a)
         tr = torch.zeros(2048 * max(args.trace, 1) * 4 + 4096 + 2048 * 32, dtype=torch.int64, device="cuda")
         for r in range(args.reps):
-            flush_l2()
+            if not args.noflush:
+                flush_l2()
             tr.zero_()
             res, st = hc.search(h, yd, stats=True, path=args.path, tile_bytes=args.tile,
                                 stages=args.stages, seg_per_lane=args.spl, time_kernel=1,
