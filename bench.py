@@ -13,9 +13,13 @@ searches of 256 MiB.  L2 is flushed (2 x L2 bytes read) before every
 search, outside the timed intervals; each search is timed with CUDA events on
 its stream.  value = bytes searched / summed search time.
 
-Under torchrun (N>1) every rank searches the same text with its own seeded
-patterns (weak scaling; no data-path collective); value = bytes
-searched by all ranks / max over ranks of the search time.
+Under torchrun (N>1), --mode replicas (default): every rank searches the same text
+with its own seeded patterns (weak scaling; no data-path collective, DESIGN.md 6);
+value = bytes searched by all ranks / max over ranks of the search time.
+--mode shard: the ranks search every pattern together, each over its share of the
+window ends (an (m-1)-byte halo on the left), and all-gather counts and positions
+over NCCL (paper_2310_15711_b200/shard.py; strong scaling); a search's
+time is its kernel time plus the exchange, value = n x searches / max over ranks.
 
 --impl reference times the oracle (oracle/, plain C HC of Fig. 5 run over the
 host cores) on a bounded sample of the same workload: the base contract's
@@ -202,6 +206,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -223,7 +228,9 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     sp = int(stream.cuda_stream)
-    y_np, work = gen_workload(cfg, rank, args.per_m)
+    shard_mode = args.mode == "shard"
+    # replicas: per-rank patterns (salt = rank); shard: every rank takes part in every search
+    y_np, work = gen_workload(cfg, 0 if shard_mode else rank, args.per_m)
     n = len(y_np)
     y = torch.from_numpy(y_np).to(dev)
     handles = [hc.prepare(x, q, a) for (m, q, a, o, x) in work]
@@ -244,6 +251,15 @@ def main():
     st = hc.Stats()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in work]
+    if shard_mode:
+        from paper_2310_15711_b200.shard import shard_bounds
+        shards = {m: shard_bounds(n, m, ws, rank) for m in cfg.ms}
+        xev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in work]
+        cnt_t = torch.zeros(1, dtype=torch.int64, device=dev)
+        pad = torch.full((cap,), -1, dtype=torch.int64, device=dev)
+        g_cnt = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
+        g_pos = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in range(ws)]
 
     def step(timed: bool):
         per = []
@@ -252,17 +268,36 @@ def main():
             flush_l2()
             e0, e1 = ev[k]
             e0.record(stream)
-            c = hc.search_raw(h, y.data_ptr(), n, pos.data_ptr(), cap, sp, opts, st)
+            if shard_mode:
+                sh = shards[work[k][0]]
+                c = hc.search_raw(h, y.data_ptr() + sh.text_lo, sh.size, pos.data_ptr(), cap, sp,
+                                  opts, st) if sh.size >= work[k][0] else 0
+                x0, x1 = xev[k]
+                x0.record(stream)
+                # exchange: counts, then the positions padded to cap
+                torch.add(pos[:c], sh.text_lo, out=pad[:c])   # global positions
+                if dist:
+                    cnt_t.fill_(c)
+                    dist.all_gather(g_cnt, cnt_t)
+                    dist.all_gather(g_pos, pad)
+                x1.record(stream)
+            else:
+                c = hc.search_raw(h, y.data_ptr(), n, pos.data_ptr(), cap, sp, opts, st)
+                assert c == counts[k]
             e1.record(stream)
-            assert c == counts[k]
             launches += st.launches
             per.append((st.kernel_ms, st.path))
+            if shard_mode and not timed:
+                total = int(sum(t.item() for t in g_cnt)) if dist else c
+                assert total == counts[k], (k, total, counts[k])
         torch.cuda.synchronize(dev)
         calls = [e0.elapsed_time(e1) for (e0, e1) in ev]
         # value uses the library's device time of each call's work (search launch to the
         # end of its last kernel, CUDA events on the launching stream); the event pair
         # around the Python call (host API overhead included) is reported as call time
         times = [kms for (kms, _) in per]
+        if shard_mode:
+            times = [t + x0.elapsed_time(x1) for t, (x0, x1) in zip(times, xev)]
         return times, per, launches, calls
 
     for _ in range(args.warmup):
@@ -291,6 +326,8 @@ def main():
 
     search_ms = sum(sum(t) for t in all_times)          # device time of all timed searches
     bytes_done = n * len(work) * args.steps
+    if shard_mode:
+        bytes_done /= ws                                 # each rank covers 1/ws of every search
     if dist:
         tt = torch.tensor([search_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -361,8 +398,11 @@ def main():
     line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(search_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "scaling": "strong" if shard_mode else "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
             "config": {"workload": cfg.name, "n": n, "ms": list(cfg.ms),
+                       "parallelism": (f"text sharded over {ws} GPUs + NCCL all-gather" if shard_mode
+                                       else f"{ws} replica(s), patterns split by rank"),
                        "patterns_per_m": len(work) // len(cfg.ms), "searches_per_step": len(work),
                        "qa": {str(m): list(cfg.qa[m]) for m in cfg.ms},
                        "l2": "flushed (2 x L2 bytes read, clean eviction) before every search, outside the timed intervals",
@@ -385,20 +425,49 @@ def main():
         h2d = n + sum(len(x) for (_, _, _, _, x) in work)
         d2h = 0
         e2e_steps = max(1, min(args.steps, 2))
+        if shard_mode:
+            # this rank's text: the union of its slices over the m values
+            lo = min(sh.text_lo for sh in shards.values())
+            hi = max(sh.text_hi for sh in shards.values())
+            h2d = (hi - lo) + sum(len(x) for (_, _, _, _, x) in work)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            ydev.copy_(y_pin, non_blocking=True)
             d2h = 0
+            if shard_mode:
+                ydev[lo:hi].copy_(y_pin[lo:hi], non_blocking=True)
+            else:
+                ydev.copy_(y_pin, non_blocking=True)
             for (m, q, a, o, x), c in zip(work, counts):
                 h = hc.prepare(x, q, a)                       # host table + upload
-                got = hc.search_raw(h, ydev.data_ptr(), n, pos.data_ptr(), cap, sp)
-                pos_pin[:got].copy_(pos[:got], non_blocking=True)
-                d2h += 8 + 8 * got
+                if shard_mode:
+                    sh = shards[m]
+                    got = hc.search_raw(h, ydev.data_ptr() + sh.text_lo, sh.size, pos.data_ptr(),
+                                        cap, sp) if sh.size >= m else 0
+                    cnt_t.fill_(got)
+                    pad[:got] = pos[:got] + sh.text_lo
+                    if dist:
+                        dist.all_gather(g_cnt, cnt_t)
+                        dist.all_gather(g_pos, pad)
+                    if rank == 0:
+                        cs = [int(t.item()) for t in g_cnt] if dist else [got]
+                        parts = [g[:k] for g, k in zip(g_pos, cs)] if dist else [pad[:got]]
+                        res = torch.cat(parts)
+                        pos_pin[:res.numel()].copy_(res, non_blocking=True)
+                        d2h += 8 * len(cs) + 8 * res.numel()
+                else:
+                    got = hc.search_raw(h, ydev.data_ptr(), n, pos.data_ptr(), cap, sp)
+                    pos_pin[:got].copy_(pos[:got], non_blocking=True)
+                    d2h += 8 + 8 * got
                 h.close()
             torch.cuda.synchronize(dev)
         t_e2e = time.perf_counter() - t0
-        line["e2e"] = {"value": round(n * len(work) * e2e_steps / t_e2e / 1e9, 1), "unit": "GB/s",
+        if dist:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e_bytes = n * len(work) * e2e_steps * (1 if shard_mode else ws)
+        line["e2e"] = {"value": round(e2e_bytes / t_e2e / 1e9, 1), "unit": "GB/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "includes": "pinned H2D of the text, hc_prepare of every pattern, hc_search, "
                                    "D2H of count and positions; wall clock"}

@@ -1,0 +1,94 @@
+"""Text-sharded HC search over several GPUs.
+
+The window ends [m-1, n) are split into `world` contiguous ranges, one per rank.
+Rank r searches only its slice of the text: y[e_lo - m + 1, e_hi), where [e_lo, e_hi)
+are its window ends.  That slice has an (m-1)-byte left halo.  By reading R11
+(segment exactness), HC on that slice reports exactly the occurrences
+whose end lies in [e_lo, e_hi).  The ranks' lists are disjoint.  Each is sorted,
+and the ranges are in rank order, so the global answer is their concatenation in
+rank order; no merge is needed.
+
+There is one exchange step, over torch.distributed (NCCL on GPUs):
+  1. all_gather of the per-rank counts (one int64 each);
+  2. all_gather of the position lists, padded to the largest count.
+Both are negligible next to each rank reading its own n/world bytes.
+
+The per-rank search is `hc.search` (the CUDA path) unless a `searcher` is passed;
+the CPU tests pass one so that the sharding and exchange logic runs under gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class Shard:
+    """Rank `rank`'s part of a text of n bytes for a pattern of length m."""
+    text_lo: int   # first text byte of the slice (the left halo starts here)
+    text_hi: int   # one past the last text byte of the slice
+    end_lo: int    # first window end owned
+    end_hi: int    # one past the last window end owned
+
+    @property
+    def size(self) -> int:
+        return self.text_hi - self.text_lo
+
+
+def shard_bounds(n: int, m: int, world: int, rank: int) -> Shard:
+    """Window ends [m-1, n) cut into `world` contiguous ranges; rank r owns the r-th.
+    An empty range yields an empty slice (size 0)."""
+    if world < 1 or not 0 <= rank < world or m < 1:
+        raise ValueError("need world >= 1, 0 <= rank < world, m >= 1")
+    W = max(0, n - m + 1)                      # number of windows
+    e_lo = m - 1 + (W * rank) // world
+    e_hi = m - 1 + (W * (rank + 1)) // world
+    if e_hi <= e_lo:
+        return Shard(e_lo, e_lo, e_lo, e_lo)
+    return Shard(e_lo - m + 1, e_hi, e_lo, e_hi)
+
+
+def gather_positions(local: torch.Tensor, group=None) -> tuple[int, torch.Tensor]:
+    """All-gather of per-rank ascending int64 position lists (already global), in rank
+    order.  Returns (total count, concatenated positions) on every rank."""
+    world = dist.get_world_size(group)
+    dev = local.device
+    cnt = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    width = max(max(counts), 1)
+    buf = torch.full((width,), -1, dtype=torch.int64, device=dev)
+    buf[:local.numel()] = local
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    pos = torch.cat([o[:c] for o, c in zip(outs, counts)])
+    return sum(counts), pos
+
+
+def _gpu_search(h, y_slice: torch.Tensor, max_out):
+    from . import hc
+    return hc.search(h, y_slice, max_out=max_out)
+
+
+def search_sharded(h, y_slice: torch.Tensor, shard: Shard, max_out: int | None = None,
+                   group=None, searcher=None) -> tuple[int, torch.Tensor]:
+    """Search this rank's slice (y_slice = y[shard.text_lo:shard.text_hi], resident on
+    this rank's device), then exchange.  Returns (count, positions) on every rank.
+    With max_out, each rank keeps its max_out smallest positions: the global
+    max_out smallest are a prefix of the rank-ordered concatenation.  The count is
+    then exact only if no rank hit max_out (the returned count is a lower bound and
+    `positions` has min(count, max_out) entries)."""
+    if y_slice.numel() != shard.size:
+        raise ValueError("y_slice does not match the shard")
+    search = searcher or _gpu_search
+    if shard.size >= h.m:
+        local = search(h, y_slice, max_out).to(torch.int64) + shard.text_lo
+    else:
+        local = torch.empty(0, dtype=torch.int64, device=y_slice.device)
+    total, pos = gather_positions(local, group)
+    if max_out is not None:
+        pos = pos[:max_out]
+    return total, pos

@@ -183,3 +183,53 @@ def test_c1_config_exact():
         assert o in want.tolist()
         for path in PATHS:
             assert np.array_equal(gpu(hc.prepare(x, q, a), yd, path=path), want)
+
+
+@pytest.mark.parametrize("world", [2, 3, 7])
+def test_text_shards_on_one_gpu(world):
+    # the shards' searches (real kernels, sliced device text with the
+    # (m-1)-byte halo), offset and concatenated in rank order, give the whole answer
+    from paper_2310_15711_b200.shard import shard_bounds
+    rng = np.random.default_rng(61 + world)
+    y = I.gen_text("dna", 1_000_003, 61)
+    for m, q in [(8, 4), (32, 6), (200, 6)]:
+        x = y[777:777 + m].copy()
+        yy = y.copy()
+        cuts = [shard_bounds(len(y), m, world, r).end_lo for r in range(1, world)]
+        for c in cuts:                       # occurrences straddling every cut
+            for d in (0, 1, m // 2, m - 1):
+                p = c - d
+                if 0 <= p <= len(y) - m:
+                    yy[p:p + m] = x
+        for p in rng.integers(0, len(y) - m, 20):
+            yy[p:p + m] = x
+        want = oracle.brute(x, yy)
+        h = hc.prepare(x, q, 12)
+        yd = to_dev(yy, 5)
+        parts = []
+        for r in range(world):
+            sh = shard_bounds(len(yy), m, world, r)
+            if sh.size >= m:
+                parts.append(gpu(h, yd[sh.text_lo:sh.text_hi]) + sh.text_lo)
+        got = np.concatenate(parts)
+        assert np.array_equal(got, want), (world, m)
+
+
+def test_search_sharded_nccl_single_rank():
+    # the exchange path over NCCL (world size 1 on the one GPU)
+    import os
+    import torch.distributed as dist
+    from paper_2310_15711_b200.shard import search_sharded, shard_bounds
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        y = I.gen_text("dna", 300_000, 62)
+        x = y[1000:1032].copy()
+        sh = shard_bounds(len(y), 32, 1, 0)
+        yd = to_dev(y)
+        total, pos = search_sharded(hc.prepare(x, 6, 12), yd[sh.text_lo:sh.text_hi], sh)
+        want = oracle.brute(x, y)
+        assert total == len(want) and np.array_equal(pos.cpu().numpy(), want)
+    finally:
+        dist.destroy_process_group()
