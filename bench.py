@@ -6,12 +6,14 @@ searched per pattern vs m on 1 B200, % of HBM peak; bit-exact).
 
 Workload (N=1): BASELINE.json configs[1] = C2, DNA-like i.i.d. text of 256 MiB,
 m in {8,...,1024}, 100 patterns per m copied from seeded text offsets, (q, alpha)
-per m from the paper's Table 1 (inputs.py).  One STEP = one hc_search call (the
-whole hot path: search kernel, count read-back, ordering of the positions into
-the caller's int64 buffer) for every (m, pattern) of the config, i.e. 800
-searches of 256 MiB.  L2 is flushed (2 x L2 bytes read) before every
-search, outside the timed intervals; each search is timed with CUDA events on
-its stream.  value = bytes searched / summed search time.
+per m from the paper's Table 1 (inputs.py).  One STEP searches every (m, pattern)
+of the config once (the whole hot path: search kernel, count read-back, ordering of
+the positions into the caller's int64 buffer), i.e. 800 searches of 256 MiB, twice:
+as one hc_search_batch call per m (the 100 searches overlap on library streams;
+`value`) and as 800 single hc_search calls (per_m single numbers, roofline).  L2 is
+flushed (2 x L2 bytes read) before every single search and every batch call,
+outside the timed intervals; the device time comes from CUDA events the library
+records on the caller's stream.  value = bytes searched / summed device time.
 
 Under torchrun (N>1), --mode replicas (default): every rank searches the same text
 with its own seeded patterns (weak scaling; no data-path collective, DESIGN.md 6);
@@ -207,6 +209,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"])
+    ap.add_argument("--api", default="batch", choices=["batch", "single"],
+                    help="value from one hc_search_batch call per m (default) or from single "
+                         "hc_search calls; both are always measured and reported per m")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -300,8 +305,30 @@ def main():
             times = [t + x0.elapsed_time(x1) for t, (x0, x1) in zip(times, xev)]
         return times, per, launches, calls
 
+    # hc_search_batch per m (all of its patterns in one call; replicas mode only)
+    use_batch = not shard_mode
+    by_m = {}
+    for k, (m, q, a, o, x) in enumerate(work):
+        by_m.setdefault(m, []).append(k)
+    if use_batch:
+        bufs = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in work]
+        bst = hc.Stats()
+
+    def batch_step(timed: bool):
+        tms = {}
+        for m, idx in by_m.items():
+            flush_l2()
+            got = hc.search_batch_raw([handles[k] for k in idx], y.data_ptr(), n,
+                                      [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp,
+                                      opts, bst)
+            assert got == [counts[k] for k in idx], m
+            tms[m] = bst.kernel_ms
+        return tms, 2 * len(work)
+
     for _ in range(args.warmup):
         step(False)
+        if use_batch:
+            batch_step(False)
 
     if dist:
         dist.barrier()
@@ -309,7 +336,9 @@ def main():
     all_times = []
     all_kernel = []
     all_calls = []
+    all_batch = []
     launches_total = 0
+    launches_batch = 0
     with Clocks(local) as clk:
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
@@ -318,6 +347,10 @@ def main():
             all_kernel.append(per)
             all_calls.append(calls)
             launches_total += launches
+            if use_batch:
+                bt, bl = batch_step(True)
+                all_batch.append(bt)
+                launches_batch += bl
         torch.cuda.synchronize(dev)
         t_wall = time.perf_counter() - t_wall0
     if dist:
@@ -325,6 +358,11 @@ def main():
     clocks = clk.summary()
 
     search_ms = sum(sum(t) for t in all_times)          # device time of all timed searches
+    value_api = "single"
+    if use_batch and args.api == "batch":
+        search_ms = sum(sum(bt.values()) for bt in all_batch)
+        value_api = "batch"
+        launches_total = launches_batch
     bytes_done = n * len(work) * args.steps
     if shard_mode:
         bytes_done /= ws                                 # each rank covers 1/ws of every search
@@ -367,6 +405,13 @@ def main():
             "q": d["q"], "alpha": d["alpha"], "path": d["path"],
             "occ_per_pattern": round(d["occ"] / len(d["t"]) * args.steps, 2),
         }
+        if use_batch:
+            bms = [bt[m] for bt in all_batch]
+            npat = len(by_m[m])
+            bmed = statistics.median(bms) / npat          # ms per pattern
+            per_m_out[str(m)]["batch_us_per_pattern"] = round(bmed * 1e3, 2)
+            per_m_out[str(m)]["batch_GBps"] = round(n / (bmed / 1e3) / 1e9, 1)
+            per_m_out[str(m)]["batch_pct_of_measured_hbm"] = round(100 * n / (bmed / 1e3) / 1e9 / peak, 1)
 
     # roofline of the dominant kernel: the staged search kernel (m whose launches take the
     # largest share of the step).  Algorithmic bytes per launch = f(m) * n +
@@ -405,11 +450,19 @@ def main():
                                        else f"{ws} replica(s), patterns split by rank"),
                        "patterns_per_m": len(work) // len(cfg.ms), "searches_per_step": len(work),
                        "qa": {str(m): list(cfg.qa[m]) for m in cfg.ms},
-                       "l2": "flushed (2 x L2 bytes read, clean eviction) before every search, outside the timed intervals",
-                       "timing": "sum over searches of the library's CUDA-event device time per "
-                                 "hc_search call (search kernel with fused count publication, plus the "
-                                 "ordering kernels when they run); per_m also gives the event time "
-                                 "around the whole Python call (host API overhead included)",
+                       "l2": "flushed (2 x L2 bytes read, clean eviction) before every single search and before every batch call, outside the timed intervals",
+                       "api": value_api,
+                       "timing": ("value: sum over m of the device time (CUDA events on the caller's "
+                                  "stream, recorded by the library) of one hc_search_batch call with "
+                                  "all of that m's patterns (the searches overlap on library streams; "
+                                  "each returns exactly its hc_search result); per_m also gives the "
+                                  "single hc_search calls (device time per call: search + finish "
+                                  "kernels) and the event time around each whole Python call")
+                                 if value_api == "batch" else
+                                 ("sum over searches of the library's CUDA-event device time per "
+                                  "hc_search call (search kernel with fused count publication, plus "
+                                  "the ordering kernels when they run); per_m also gives the event "
+                                  "time around the whole Python call (host API overhead included)"),
                        "wall_ms_per_step_incl_flush": round(1000 * t_wall / args.steps, 2),
                        "text_sha256": I.sha256(y_np)[:16]},
             "pct_of_measured_hbm": round(100 * value / peak, 1),
@@ -438,6 +491,17 @@ def main():
                 ydev[lo:hi].copy_(y_pin[lo:hi], non_blocking=True)
             else:
                 ydev.copy_(y_pin, non_blocking=True)
+            if use_batch and args.api == "batch":
+                for m, idx in by_m.items():
+                    hs = [hc.prepare(work[k][4], work[k][1], work[k][2]) for k in idx]
+                    got = hc.search_batch_raw(hs, ydev.data_ptr(), n,
+                                              [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp)
+                    for k, c in zip(idx, got):
+                        pos_pin[:c].copy_(bufs[k][:c], non_blocking=True)
+                        d2h += 8 + 8 * c
+                    for h in hs:
+                        h.close()
+                continue
             for (m, q, a, o, x), c in zip(work, counts):
                 h = hc.prepare(x, q, a)                       # host table + upload
                 if shard_mode:
@@ -469,8 +533,10 @@ def main():
         e2e_bytes = n * len(work) * e2e_steps * (1 if shard_mode else ws)
         line["e2e"] = {"value": round(e2e_bytes / t_e2e / 1e9, 1), "unit": "GB/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "includes": "pinned H2D of the text, hc_prepare of every pattern, hc_search, "
-                                   "D2H of count and positions; wall clock"}
+                       "includes": "pinned H2D of the text, hc_prepare of every pattern, "
+                                   + ("hc_search_batch per m" if (use_batch and args.api == "batch")
+                                      else "hc_search per pattern")
+                                   + ", D2H of counts and positions; wall clock"}
 
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, y_np, work, args.cpu_seconds)

@@ -129,6 +129,26 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
                      size_t max_out, cudaStream_t stream, const hc_search_opts *opts,
                      hc_search_stats *stats);
 
+/* Batch of independent searches over the same text (multi-pattern
+ * batching): the result of pattern i is exactly hc_search(hs[i], y_dev, n, pos_out[i],
+ * max_out[i], stream) (Fig. 5, per pattern).  The searches are spread over
+ * a few library-owned streams so that one pattern's tail and launch latency overlap
+ * the next pattern's work; the call is ordered after prior work on `stream`, and
+ * returns after all of them completed (stream order is preserved for later work).
+ *   hs      : npat handles (same device), read-only.
+ *   y_dev   : DEVICE text, n bytes, caller-owned, read-only.
+ *   counts  : HOST int64[npat], receives each pattern's occurrence count.
+ *   pos_out : HOST array of npat DEVICE int64 pointers (entries may be NULL), or NULL:
+ *             min(count, max_out[i]) smallest positions of pattern i, ascending.
+ *   max_out : HOST size_t[npat], or NULL (count only).
+ *   opts    : path/tuning knobs as for hc_search_ex (debug and trace are ignored);
+ *             time_kernel = 1 puts the device time of the whole batch in stats->kernel_ms.
+ * Patterns whose positions need more room than the scratch or the large sort are
+ * re-run alone (stats->reruns).  Returns HC_OK or a negative hc_status. */
+int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_dev, size_t n,
+                    int64_t *counts, int64_t *const *pos_out, const size_t *max_out,
+                    cudaStream_t stream, const hc_search_opts *opts, hc_search_stats *stats);
+
 /* End-to-end convenience: y_host and pos_out_host are HOST pointers.  Copies y to the
  * device (staged through pinned buffers when y_host is pageable), searches, and copies
  * min(count, max_out) positions back.  Synchronous.  Returns the count or a negative

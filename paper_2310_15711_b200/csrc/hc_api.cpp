@@ -170,6 +170,135 @@ constexpr uint32_t kDefaultStages = 2;
 constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
 constexpr uint32_t kDefaultSegPerLane = 2;
 
+// Launch parameters and path of one search (hc_search_ex and hc_search_batch).
+int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc_search_opts &o,
+                 hc::KParams &p, int &path) {
+    const uint32_t m = h->m, q = h->q;
+    const uint32_t S = m - q + 1;
+    const uint32_t windows = nn - m + 1;
+    const uint32_t K = (windows + S - 1) / S;
+    p = hc::KParams{};
+    p.y = y_dev;
+    p.n = nn;
+    p.F = h->dF;
+    p.x = h->dx;
+    p.m = m;
+    p.q = q;
+    p.s = h->s;
+    p.mask = h->mask;
+    p.hv = h->hv;
+    p.S = S;
+    p.alpha = h->alpha;
+    p.K = K;
+    p.debug = static_cast<uint32_t>(o.debug);
+    p.tma_chunk = o.tma_chunk > 0 ? (static_cast<uint32_t>(o.tma_chunk) + 15) & ~15u : 0u;
+    p.trace = o.trace;
+    p.trace_tiles = o.trace_tiles > 0 ? static_cast<uint32_t>(o.trace_tiles) : 0u;
+
+    path = o.path;
+    if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STAGED : HC_PATH_GATHER;
+    if (path == HC_PATH_STAGED) {
+        uint32_t stage = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultStageBytes;
+        // at least 32 segments (one per lane of a warp) per tile
+        const uint32_t need = 32 * S + m + 48;
+        if (stage < need) stage = need;
+        stage = (stage + 15) & ~15u;
+        // an even number (2..16): each of the 2 survivor warps owns every other
+        // iteration, hence the tile chains of half the stages
+        p.stages = o.stages > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.stages) + 1u) & ~1u
+                                : kDefaultStages;
+        p.stage_bytes = stage;
+        // segments whose bytes [k0*S, m-1+k1*S) fit with 16 B of misalignment slack at
+        // each end: (k1-k0)*S + m - 1 + 32 <= stage
+        p.seg_per_tile = (stage - 32 - (m - 1)) / S;
+        p.ntiles = (K + p.seg_per_tile - 1) / p.seg_per_tile;
+        // survivor boxes of the survivor warps: a segment's text (<= m + S - 1 bytes)
+        // in whole 16-byte chunks, as many as fit next to the stages for 3 CTAs per SM
+        p.slot_bytes = 16 * ((m + S + 29) / 16);
+        {
+            const uint32_t fixed = static_cast<uint32_t>(
+                hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, 0)) + 16;
+            const uint32_t room = fixed < kStagedSmem3 ? kStagedSmem3 - fixed : 0u;
+            p.nbox = std::min<uint32_t>(64u, room / (2 * (p.slot_bytes + 8)));
+        }
+        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
+        if (smem > max_smem_optin(h->device)) {
+            if (o.path == HC_PATH_STAGED) return HC_EINVAL;
+            path = HC_PATH_GATHER;
+        }
+    }
+    if (path == HC_PATH_GATHER) {
+        const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)
+                                                : (S >= 512 ? 1u : kDefaultSegPerLane);
+        p.seg_per_chunk = 32 * spl;
+        p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
+        if (hc::gather_smem_bytes(p.alpha, m) > max_smem_optin(h->device)) return HC_EINVAL;
+    }
+
+    return HC_OK;
+}
+
+// hc_search_batch resources, per host thread and device: kBatchStreams non-blocking
+// streams, each with its own scratch (counter + positions), and a mapped pinned array
+// the finish kernels write the patterns' counts into.
+constexpr int kBatchStreams = 4;
+struct BatchRes {
+    cudaStream_t st[kBatchStreams] = {};
+    cudaEvent_t ev[kBatchStreams + 1] = {};
+    Scratch sc[kBatchStreams];
+    uint32_t *hcounts = nullptr, *hcounts_dev = nullptr;
+    size_t ncounts = 0;
+};
+thread_local BatchRes g_batch[8];
+
+cudaError_t batch_scratch(Scratch &sc, size_t cap) {
+    if (!sc.buf || sc.cap < cap) {
+        if (sc.buf) cudaFree(sc.buf);
+        sc.buf = nullptr;
+        cudaError_t e = cudaMalloc(&sc.buf, 16 + cap * sizeof(uint32_t));
+        if (e != cudaSuccess) {
+            sc.cap = 0;
+            return e;
+        }
+        e = cudaMemset(sc.buf, 0, 16);
+        if (e != cudaSuccess) return e;
+        sc.cap = cap;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t batch_res(int dev, size_t npat, BatchRes **out) {
+    if (dev < 0 || dev >= 8) return cudaErrorInvalidDevice;
+    BatchRes &r = g_batch[dev];
+    if (!r.st[0]) {
+        for (int i = 0; i < kBatchStreams; ++i) {
+            cudaError_t e = cudaStreamCreateWithFlags(&r.st[i], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return e;
+        }
+        for (int i = 0; i <= kBatchStreams; ++i) {
+            cudaError_t e = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    if (r.ncounts < npat) {
+        if (r.hcounts) cudaFreeHost(r.hcounts);
+        r.hcounts = nullptr;
+        r.ncounts = 0;
+        void *hp = nullptr;
+        const size_t want = std::max<size_t>(npat, 256);
+        cudaError_t e = cudaHostAlloc(&hp, want * 4, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return e;
+        void *dp = nullptr;
+        e = cudaHostGetDevicePointer(&dp, hp, 0);
+        if (e != cudaSuccess) return e;
+        r.hcounts = static_cast<uint32_t *>(hp);
+        r.hcounts_dev = static_cast<uint32_t *>(dp);
+        r.ncounts = want;
+    }
+    *out = &r;
+    return cudaSuccess;
+}
+
 }  // namespace
 
 extern "C" {
@@ -284,61 +413,10 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     const uint32_t K = (windows + S - 1) / S;
 
     hc::KParams p{};
-    p.y = y_dev;
-    p.n = nn;
-    p.F = h->dF;
-    p.x = h->dx;
-    p.m = m;
-    p.q = q;
-    p.s = h->s;
-    p.mask = h->mask;
-    p.hv = h->hv;
-    p.S = S;
-    p.alpha = h->alpha;
-    p.K = K;
-    p.debug = static_cast<uint32_t>(o.debug);
-    p.tma_chunk = o.tma_chunk > 0 ? (static_cast<uint32_t>(o.tma_chunk) + 15) & ~15u : 0u;
-    p.trace = o.trace;
-    p.trace_tiles = o.trace_tiles > 0 ? static_cast<uint32_t>(o.trace_tiles) : 0u;
-
-    int path = o.path;
-    if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STAGED : HC_PATH_GATHER;
-    if (path == HC_PATH_STAGED) {
-        uint32_t stage = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultStageBytes;
-        // at least 32 segments (one per lane of a warp) per tile
-        const uint32_t need = 32 * S + m + 48;
-        if (stage < need) stage = need;
-        stage = (stage + 15) & ~15u;
-        // an even number (2..16): each of the 2 survivor warps owns every other
-        // iteration, hence the tile chains of half the stages
-        p.stages = o.stages > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.stages) + 1u) & ~1u
-                                : kDefaultStages;
-        p.stage_bytes = stage;
-        // segments whose bytes [k0*S, m-1+k1*S) fit with 16 B of misalignment slack at
-        // each end: (k1-k0)*S + m - 1 + 32 <= stage
-        p.seg_per_tile = (stage - 32 - (m - 1)) / S;
-        p.ntiles = (K + p.seg_per_tile - 1) / p.seg_per_tile;
-        // survivor boxes of the survivor warps: a segment's text (<= m + S - 1 bytes)
-        // in whole 16-byte chunks, as many as fit next to the stages for 3 CTAs per SM
-        p.slot_bytes = 16 * ((m + S + 29) / 16);
-        {
-            const uint32_t fixed = static_cast<uint32_t>(
-                hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, 0)) + 16;
-            const uint32_t room = fixed < kStagedSmem3 ? kStagedSmem3 - fixed : 0u;
-            p.nbox = std::min<uint32_t>(64u, room / (2 * (p.slot_bytes + 8)));
-        }
-        const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
-        if (smem > max_smem_optin(h->device)) {
-            if (o.path == HC_PATH_STAGED) return fail(HC_EINVAL);
-            path = HC_PATH_GATHER;
-        }
-    }
-    if (path == HC_PATH_GATHER) {
-        const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)
-                                                : (S >= 512 ? 1u : kDefaultSegPerLane);
-        p.seg_per_chunk = 32 * spl;
-        p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
-        if (hc::gather_smem_bytes(p.alpha, m) > max_smem_optin(h->device)) return fail(HC_EINVAL);
+    int path = 0;
+    {
+        const int rc = setup_search(h, y_dev, nn, o, p, path);
+        if (rc != HC_OK) return fail(rc);
     }
 
     // scratch: [counter | positions]
@@ -372,7 +450,11 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         if (e == cudaSuccess) {
             stage = "finish kernel launch";
             *sc->host_count = 0xffffffffu;
-            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, sc->host_count_dev, stream);
+            // debug trace: the finish kernel's start / after-wait stamps follow the CTA stamps
+            unsigned long long *ftr = nullptr;
+            if (o.trace) ftr = o.trace + static_cast<size_t>(li.grid) * p.trace_tiles * 4 + 2 * li.grid;
+            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, sc->host_count_dev, stream,
+                                  ftr);
             ++launches;
         }
         // device time of the call: search + finish (count publication, ordering of up to
@@ -433,6 +515,117 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         stats->kernel_ms = kms;
     }
     return static_cast<int64_t>(count);
+}
+
+int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_dev, size_t n,
+                    int64_t *counts, int64_t *const *pos_out, const size_t *max_out,
+                    cudaStream_t stream, const hc_search_opts *opts, hc_search_stats *stats) {
+    if (npat == 0) return HC_OK;
+    if (!hs || !counts || (n > 0 && !y_dev)) return fail(HC_EINVAL);
+    if (n > HC_MAX_TEXT) return fail(HC_ETOOLONG);
+    hc_search_opts o{};
+    if (opts) o = *opts;
+    o.debug = 0;
+    o.trace = nullptr;
+    if (stats) *stats = hc_search_stats{};
+    g_last_error = HC_OK;
+    const int dev = hs[0] ? hs[0]->device : -1;
+    for (size_t i = 0; i < npat; ++i)
+        if (!hs[i] || hs[i]->device != dev) return fail(HC_EINVAL);
+    DeviceGuard guard(dev);
+    tune_pool(dev);
+    BatchRes *r = nullptr;
+    cudaError_t e = batch_res(dev, npat, &r);
+    if (e != cudaSuccess) return cuda_fail(e, "batch resources");
+    const uint32_t nn = static_cast<uint32_t>(n);
+
+    // the pool streams start after the caller's stream (y_dev is ready there)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (o.time_kernel) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, stream);
+    }
+    cudaEventRecord(r->ev[kBatchStreams], stream);
+    for (int j = 0; j < kBatchStreams; ++j) cudaStreamWaitEvent(r->st[j], r->ev[kBatchStreams], 0);
+
+    std::vector<uint8_t> redo(npat, 0);
+    std::vector<size_t> caps(npat, 0);
+    int launches = 0;
+    for (size_t i = 0; i < npat; ++i) {
+        const hc_handle *h = hs[i];
+        r->hcounts[i] = 0xffffffffu;
+        if (n < h->m) {
+            r->hcounts[i] = 0;
+            continue;
+        }
+        const size_t windows = n - h->m + 1;
+        const size_t mo = max_out ? max_out[i] : 0;
+        const bool want_pos = pos_out && pos_out[i] && mo > 0;
+        hc::KParams p{};
+        int path = 0;
+        const int rc = setup_search(h, y_dev, nn, o, p, path);
+        if (rc != HC_OK) return fail(rc);
+        const int j = static_cast<int>(i % kBatchStreams);
+        Scratch &sc = r->sc[j];
+        const size_t cap = want_pos ? std::min<size_t>(std::max<size_t>(mo, size_t(1) << 16), windows) : 0;
+        e = batch_scratch(sc, std::max<size_t>(cap, 1));
+        if (e != cudaSuccess) return cuda_fail(e, "batch scratch");
+        caps[i] = cap;
+        p.counter = sc.buf;
+        p.out = want_pos ? sc.buf + 4 : nullptr;
+        p.cap = static_cast<uint32_t>(cap);
+        hc::LaunchInfo li;
+        e = path == HC_PATH_STAGED ? hc::launch_staged(p, r->st[j], o.max_ctas, o.ctas_per_sm, &li)
+                                   : hc::launch_gather(p, r->st[j], o.max_ctas, o.ctas_per_sm, &li);
+        if (e == cudaSuccess)
+            e = hc::launch_finish(sc.buf, p.out, p.cap, want_pos ? pos_out[i] : nullptr,
+                                  want_pos ? static_cast<uint32_t>(std::min<size_t>(mo, windows)) : 0u,
+                                  r->hcounts_dev + i, r->st[j]);
+        if (e != cudaSuccess) return cuda_fail(e, "batch launch");
+        launches += 2;
+    }
+    for (int j = 0; j < kBatchStreams; ++j) {
+        cudaEventRecord(r->ev[j], r->st[j]);
+        cudaStreamWaitEvent(stream, r->ev[j], 0);
+    }
+    if (o.time_kernel) cudaEventRecord(ev1, stream);
+    e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+        for (int j = 0; j < kBatchStreams; ++j) {   // counters may be left non-zero
+            cudaFree(r->sc[j].buf);
+            r->sc[j].buf = nullptr;
+            r->sc[j].cap = 0;
+        }
+        return cuda_fail(e, "batch execution");
+    }
+    float kms = 0.f;
+    if (o.time_kernel) {
+        cudaEventElapsedTime(&kms, ev0, ev1);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+    }
+    // patterns whose positions did not fit the scratch or need the large sort are run
+    // again on their own (their counts are exact already)
+    int reruns = 0;
+    for (size_t i = 0; i < npat; ++i) {
+        const uint32_t c = reinterpret_cast<volatile uint32_t *>(r->hcounts)[i];
+        counts[i] = c;
+        const size_t mo = max_out ? max_out[i] : 0;
+        const bool want_pos = pos_out && pos_out[i] && mo > 0;
+        if (want_pos && c > 0 && (c > caps[i] || c > hc::kSmallSort)) {
+            const int64_t c2 = hc_search_ex(hs[i], y_dev, n, pos_out[i], mo, stream, &o, nullptr);
+            if (c2 < 0) return static_cast<int>(c2);
+            counts[i] = c2;
+            ++reruns;
+        }
+    }
+    if (stats) {
+        stats->launches = launches;
+        stats->reruns = reruns;
+        stats->kernel_ms = kms;
+    }
+    return HC_OK;
 }
 
 int64_t hc_search(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t *pos_out,

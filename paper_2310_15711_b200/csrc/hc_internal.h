@@ -50,7 +50,8 @@ cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int c
 // One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,
 // ordering of <= kSmallSort positions into dst (first min(count, max_out), int64).
 cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
-                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st);
+                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st,
+                          unsigned long long *trace = nullptr);
 // Ordering of count > kSmallSort positions (CUB radix sort), first k written as int64.
 cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
                        uint32_t k, cudaStream_t st, int *launches);

@@ -1084,6 +1084,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) trace_cta(p, 0);
     pdl_launch_dependents();
     load_table(p, sFp, sx);
     if (tid == 0) s_params = p;
@@ -1103,6 +1104,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     }
     sink.drain();
     wo.flush(p, lane);
+    if (lane == 0) trace_cta(p, 1);   // last warp to get here wins
 }
 
 // ------------------------------------------------------------------ launchers
@@ -1233,9 +1235,12 @@ __global__ void widen_kernel(const uint32_t *src, int64_t *dst, uint32_t k) {
 __global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const uint32_t *pos,
                                                       uint32_t cap, int64_t *dst,
                                                       uint32_t max_out,
-                                                      volatile uint32_t *host_count) {
+                                                      volatile uint32_t *host_count,
+                                                      unsigned long long *trace) {
     __shared__ uint32_t s[kSmallSort];
+    if (trace && threadIdx.x == 0) trace[0] = gtimer();
     pdl_wait();   // the search grid has completed and its writes are visible
+    if (trace && threadIdx.x == 0) trace[1] = gtimer();
     const uint32_t count = *counter;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1273,7 +1278,8 @@ __global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const u
 }
 
 cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
-                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st) {
+                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st,
+                          unsigned long long *trace) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(1);
     cfg.blockDim = dim3(1024);
@@ -1285,7 +1291,7 @@ cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, finish_kernel, counter, pos, cap, dst, max_out,
-                              host_count_dev);
+                              host_count_dev, trace);
 }
 
 // count > kSmallSort: CUB radix sort on ceil(log2 n) bits, then widen the first k.

@@ -33,7 +33,8 @@ WORD_BITS = 32
 
 # the symbols include/hc.h declares (tests check every one is exported)
 EXPORTS = ("hc_prepare", "hc_last_error", "hc_strerror", "hc_search", "hc_search_ex",
-           "hc_search_host", "hc_destroy", "hc_table", "hc_build_table", "hc_version")
+           "hc_search_batch", "hc_search_host", "hc_destroy", "hc_table", "hc_build_table",
+           "hc_version")
 
 
 class Opts(C.Structure):
@@ -66,6 +67,11 @@ _lib.hc_search.restype = C.c_int64
 _lib.hc_search_ex.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                               C.c_void_p, C.POINTER(Opts), C.POINTER(Stats)]
 _lib.hc_search_ex.restype = C.c_int64
+_lib.hc_search_batch.argtypes = [C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.c_size_t,
+                                 C.POINTER(C.c_int64), C.POINTER(C.c_void_p),
+                                 C.POINTER(C.c_size_t), C.c_void_p, C.POINTER(Opts),
+                                 C.POINTER(Stats)]
+_lib.hc_search_batch.restype = C.c_int
 _lib.hc_search_host.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                                 C.c_void_p]
 _lib.hc_search_host.restype = C.c_int64
@@ -220,6 +226,44 @@ def search(h: Handle, y, max_out: int | None = None, stream=None, stats: bool = 
             out = torch.empty(cnt, dtype=torch.int64, device=y.device)
             cnt = search_raw(h, y.data_ptr(), n, out.data_ptr(), cnt, st, o, S)
         res = out[:cnt]
+    return (res, S.as_dict()) if stats else res
+
+
+def search_batch_raw(handles, y_ptr: int, n: int, pos_ptrs, max_outs, stream_ptr: int,
+                     opts: Opts | None = None, stats: Stats | None = None) -> list[int]:
+    """hc_search_batch on raw pointers: pos_ptrs / max_outs are per-pattern lists (or
+    None for count only); returns the counts (raises on error)."""
+    P = len(handles)
+    hs = (C.c_void_p * P)(*[h.ptr.value for h in handles])
+    counts = (C.c_int64 * P)()
+    pp = (C.c_void_p * P)(*pos_ptrs) if pos_ptrs is not None else None
+    mo = (C.c_size_t * P)(*max_outs) if max_outs is not None else None
+    rc = _lib.hc_search_batch(hs, P, C.c_void_p(y_ptr), n, counts, pp, mo, C.c_void_p(stream_ptr),
+                              C.byref(opts) if opts is not None else None,
+                              C.byref(stats) if stats is not None else None)
+    if rc != HC_OK:
+        raise HCError(int(rc), "hc_search_batch")
+    return list(counts)
+
+
+def search_batch(handles, y, max_out: int | None = None, stream=None, stats: bool = False, **kw):
+    """Searches every handle's pattern in the uint8 CUDA tensor y with one
+    hc_search_batch call; returns a list of int64 CUDA tensors (as search() would).
+    With max_out=None the results are exact (counts first, then the positions)."""
+    import torch
+    assert y.dtype == torch.uint8 and y.is_cuda and y.is_contiguous()
+    n = y.numel()
+    st = _stream_ptr(stream)
+    o = _opts(**kw) if kw else None
+    S = Stats() if stats else None
+    if max_out is None:
+        cnts = search_batch_raw(handles, y.data_ptr(), n, None, None, st, o, None)
+        mos = [max(c, 1) for c in cnts]
+    else:
+        mos = [max(int(max_out), 1)] * len(handles)
+    outs = [torch.empty(k, dtype=torch.int64, device=y.device) for k in mos]
+    cnts = search_batch_raw(handles, y.data_ptr(), n, [t.data_ptr() for t in outs], mos, st, o, S)
+    res = [t[:min(c, k)] for t, c, k in zip(outs, cnts, mos)]
     return (res, S.as_dict()) if stats else res
 
 

@@ -233,3 +233,35 @@ def test_search_sharded_nccl_single_rank():
         assert total == len(want) and np.array_equal(pos.cpu().numpy(), want)
     finally:
         dist.destroy_process_group()
+
+
+def test_search_batch_matches_single_searches():
+    # hc_search_batch: every pattern's result is exactly hc_search's,
+    # with mixed m / q / alpha / paths, zero and high occurrence counts (re-runs)
+    rng = np.random.default_rng(71)
+    y = I.gen_text("dna", 2_000_003, 71)
+    yy = y.copy()
+    specs = [(8, 4, 12), (16, 6, 12), (32, 6, 12), (33, 3, 11), (64, 6, 12), (200, 6, 12),
+             (512, 6, 12), (1024, 8, 12), (5, 5, 10), (3, 2, 8)]
+    pats = []
+    for m, q, a in specs:
+        o = int(rng.integers(0, len(y) - m))
+        x = y[o:o + m].copy()
+        for p in rng.integers(0, len(y) - m, 7):
+            yy[p:p + m] = x
+        pats.append((x, q, a))
+    pats.append((np.frombuffer(b"ZZZZZZZZZZ", np.uint8), 3, 12))      # absent
+    yd = to_dev(yy, 9)
+    hs = [hc.prepare(x, q, a) for x, q, a in pats]
+    want = [oracle.brute(x, yy) for x, _, _ in pats]
+    got = hc.search_batch(hs, yd)
+    torch.cuda.synchronize()
+    for g, w in zip(got, want):
+        assert np.array_equal(g.cpu().numpy(), w)
+    # max_out truncation and counts; a tiny scratch forces the re-run path for m=3
+    got, st = hc.search_batch(hs, yd, max_out=5, stats=True, time_kernel=1)
+    for g, w in zip(got, want):
+        assert np.array_equal(g.cpu().numpy(), w[:5])
+    assert st["kernel_ms"] > 0
+    cnts = hc.search_batch_raw(hs, yd.data_ptr(), yd.numel(), None, None, 0)
+    assert cnts == [len(w) for w in want]

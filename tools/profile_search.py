@@ -19,7 +19,8 @@ from paper_2310_15711_b200 import inputs as I  # noqa: E402
 def analyze_trace(tr, grid, T, stages):
     import numpy as np
     a = tr[:grid * T * 4].view(grid, T, 4).cpu().numpy().astype(np.float64)
-    t0 = a[a > 0].min()
+    ce0 = tr[grid * T * 4: grid * T * 4 + 2 * grid].view(grid, 2).cpu().numpy().astype(np.float64)
+    t0 = a[a > 0].min() if (a > 0).any() else ce0[ce0 > 0].min()
     a = np.where(a > 0, a - t0, np.nan) / 1e3   # us since first event
     fs, fe, se, ss = a[..., 0], a[..., 1], a[..., 2], a[..., 3]
     med = lambda v: float(np.nanmedian(v)) if np.isfinite(v).any() else float("nan")
@@ -31,6 +32,10 @@ def analyze_trace(tr, grid, T, stages):
     ce = (ce - t0) / 1e3
     print(f"  CTA entry min {ce[:, 0].min():.2f} p50 {np.median(ce[:, 0]):.2f} max {ce[:, 0].max():.2f}; "
           f"exit p50 {np.median(ce[:, 1]):.2f} max {ce[:, 1].max():.2f} (us vs first tile event)")
+    fz = tr[grid * T * 4 + 2 * grid: grid * T * 4 + 2 * grid + 2].cpu().numpy().astype(np.float64)
+    fz = (fz - t0) / 1e3
+    print(f"  finish kernel: start {fz[0]:.2f}, after griddepcontrol.wait {fz[1]:.2f}; "
+          f"grid span (first entry -> finish wait) {fz[1] - ce[:, 0].min():.2f} us")
     last = np.nanmax(np.where(np.isfinite(fe), fe, np.nan), axis=1)   # per CTA, last traced filter end
     print(f"  span: first event 0, CTA last-traced-filter-end p50 {np.nanpercentile(last, 50):.2f} "
           f"p90 {np.nanpercentile(last, 90):.2f} max {np.nanmax(last):.2f} us; "
