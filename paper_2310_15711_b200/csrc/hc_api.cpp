@@ -241,7 +241,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
 // hc_search_batch resources, per host thread and device: kBatchStreams non-blocking
 // streams, each with its own scratch (counter + positions), and a mapped pinned array
 // the finish kernels write the patterns' counts into.
-constexpr int kBatchStreams = 4;
+constexpr int kBatchStreams = 8;
 struct BatchRes {
     cudaStream_t st[kBatchStreams] = {};
     cudaEvent_t ev[kBatchStreams + 1] = {};
