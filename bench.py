@@ -40,6 +40,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+PATH_NAMES = {1: "staged", 2: "gather", 3: "stream"}
 sys.path.insert(0, ROOT)
 
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
@@ -387,7 +388,7 @@ def main():
             d["t"].append(all_times[s][k])
             d["kt"].append(all_kernel[s][k][0])
             d["ct"].append(all_calls[s][k])
-        d["path"] = "staged" if all_kernel[0][k][1] == hc.PATH_STAGED else "gather"
+        d["path"] = PATH_NAMES[all_kernel[0][k][1]]
         d["occ"] += counts[k]
     per_m_out = {}
     for m, d in per_m.items():
@@ -413,8 +414,8 @@ def main():
             per_m_out[str(m)]["batch_GBps"] = round(n / (bmed / 1e3) / 1e9, 1)
             per_m_out[str(m)]["batch_pct_of_measured_hbm"] = round(100 * n / (bmed / 1e3) / 1e9 / peak, 1)
 
-    # roofline of the dominant kernel: the staged search kernel (m whose launches take the
-    # largest share of the step).  Algorithmic bytes per launch = f(m) * n +
+    # roofline of the dominant kernel: the search kernel whose launches take the largest
+    # share of the step (the stream kernel on C2: m <= 32).  Algorithmic bytes per launch = f(m) * n +
     # 4 B per position written.
     shares = {}
     for m, d in per_m.items():
@@ -423,7 +424,7 @@ def main():
     alg_bytes = 0.0
     kt = 0.0
     for k, (m, q, a, o, x) in enumerate(work):
-        path = "staged" if all_kernel[0][k][1] == hc.PATH_STAGED else "gather"
+        path = PATH_NAMES[all_kernel[0][k][1]]
         if path != dom:
             continue
         for s in range(args.steps):
@@ -493,6 +494,7 @@ def main():
                 ydev.copy_(y_pin, non_blocking=True)
             if use_batch and args.api == "batch":
                 for m, idx in by_m.items():
+                    t_m = time.perf_counter()
                     hs = [hc.prepare(work[k][4], work[k][1], work[k][2]) for k in idx]
                     got = hc.search_batch_raw(hs, ydev.data_ptr(), n,
                                               [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp)
@@ -501,6 +503,9 @@ def main():
                         d2h += 8 + 8 * c
                     for h in hs:
                         h.close()
+                    if os.environ.get("HC_BENCH_DEBUG"):
+                        torch.cuda.synchronize(dev)
+                        print(f"e2e m={m}: {1e3 * (time.perf_counter() - t_m):.2f} ms", file=sys.stderr)
                 continue
             for (m, q, a, o, x), c in zip(work, counts):
                 h = hc.prepare(x, q, a)                       # host table + upload

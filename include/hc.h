@@ -89,13 +89,15 @@ int64_t hc_search(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t *p
 typedef enum hc_path {
     HC_PATH_AUTO = 0,   /* chosen from m, q */
     HC_PATH_STAGED = 1, /* text tiles staged in shared memory by TMA bulk copies */
-    HC_PATH_GATHER = 2  /* no staging: lanes read only the q-grams they hash, from global memory */
+    HC_PATH_GATHER = 2, /* no staging: lanes read only the q-grams they hash, from global memory */
+    HC_PATH_STREAM = 3  /* per-warp chunks staged in shared memory by 16-byte cp.async copies */
 } hc_path;
 
 typedef struct hc_search_opts {
     int path;         /* hc_path */
-    int tile_bytes;   /* staged: text bytes per shared-memory stage (0 = default) */
-    int stages;       /* staged: TMA pipeline depth (0 = default) */
+    int tile_bytes;   /* staged: text bytes per shared-memory stage; stream: target text bytes
+                         per warp chunk (0 = default) */
+    int stages;       /* staged: TMA pipeline depth; stream: buffers per warp, 2..4 (0 = default) */
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
     int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms) */

@@ -159,9 +159,11 @@ int max_smem_optin(int dev) {
     return v > 0 ? v : 48 * 1024;
 }
 
-// Default path choice: stage the whole text when the shift is small
-// (the lattice is dense and filtering from shared memory pays); gather otherwise.
-// Measured on C2 (B200): staged ahead up to m = 32 (S = 27), gather from m = 48.
+// Default path choice: stream the whole text through per-warp shared
+// buffers when the shift is small (the lattice is dense, every sector is read);
+// gather otherwise.  Measured on C2 (B200): the stream path leads the staged (TMA
+// ring) path at every m <= 64 and the gather path up to m = 32 (S = 27); gather leads
+// from m = 128, and m = 64 is a tie.
 constexpr uint32_t kStagedMaxShift = 32;
 constexpr uint32_t kDefaultStageBytes = 24576;
 constexpr uint32_t kDefaultStages = 2;
@@ -169,6 +171,17 @@ constexpr uint32_t kDefaultStages = 2;
 // reserved per CTA, 1.3 KB static
 constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
 constexpr uint32_t kDefaultSegPerLane = 2;
+constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per warp chunk
+constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
+
+cudaError_t launch_search(int path, const hc::KParams &p, cudaStream_t st, const hc_search_opts &o,
+                          hc::LaunchInfo *li) {
+    switch (path) {
+    case HC_PATH_STAGED: return hc::launch_staged(p, st, o.max_ctas, o.ctas_per_sm, li);
+    case HC_PATH_STREAM: return hc::launch_stream(p, st, o.max_ctas, o.ctas_per_sm, li);
+    default: return hc::launch_gather(p, st, o.max_ctas, o.ctas_per_sm, li);
+    }
+}
 
 // Launch parameters and path of one search (hc_search_ex and hc_search_batch).
 int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc_search_opts &o,
@@ -196,7 +209,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
     p.trace_tiles = o.trace_tiles > 0 ? static_cast<uint32_t>(o.trace_tiles) : 0u;
 
     path = o.path;
-    if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STAGED : HC_PATH_GATHER;
+    if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STREAM : HC_PATH_GATHER;
     if (path == HC_PATH_STAGED) {
         uint32_t stage = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultStageBytes;
         // at least 32 segments (one per lane of a warp) per tile
@@ -226,6 +239,21 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
             if (o.path == HC_PATH_STAGED) return HC_EINVAL;
             path = HC_PATH_GATHER;
         }
+    }
+    if (path == HC_PATH_STREAM) {
+        const uint32_t target = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultChunkBytes;
+        // a multiple of 32 * kUnroll segments, so the filter runs full unrolled steps
+        // (of 32 for large shifts)
+        const uint32_t unit = S <= 32 ? 128u : 32u;
+        p.seg_per_chunk = unit * std::max<uint32_t>(1u, (target / S + unit / 2) / unit);
+        p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
+        // chunk bytes [k0 S + S - 1, k1 S + q - 2] plus 16-byte alignment slack
+        p.stage_bytes = (p.seg_per_chunk * S + q + 32 + 15) & ~15u;
+        p.stages = o.stages >= 2 && o.stages <= 4 ? static_cast<uint32_t>(o.stages) : kDefaultStreamBufs;
+        // shifts too long for per-warp buffers (S > ~200) take the gather path, which
+        // reads only the q-grams it hashes anyway
+        if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages) > max_smem_optin(h->device))
+            path = HC_PATH_GATHER;
     }
     if (path == HC_PATH_GATHER) {
         const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)
@@ -443,8 +471,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             cudaEventRecord(ev0, stream);
         }
         const char *stage = "search kernel launch";
-        e = path == HC_PATH_STAGED ? hc::launch_staged(p, stream, o.max_ctas, o.ctas_per_sm, &li)
-                                   : hc::launch_gather(p, stream, o.max_ctas, o.ctas_per_sm, &li);
+        e = launch_search(path, p, stream, o, &li);
         ++launches;
         if (timed && o.debug == 7) cudaEventRecord(ev1, stream);   // search kernel alone
         if (e == cudaSuccess) {
@@ -453,7 +480,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             // debug trace: the finish kernel's start / after-wait stamps follow the CTA stamps
             unsigned long long *ftr = nullptr;
             if (o.trace) ftr = o.trace + static_cast<size_t>(li.grid) * p.trace_tiles * 4 + 2 * li.grid;
-            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, sc->host_count_dev, stream,
+            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, p.n, sc->host_count_dev, stream,
                                   ftr);
             ++launches;
         }
@@ -576,12 +603,11 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
         p.out = want_pos ? sc.buf + 4 : nullptr;
         p.cap = static_cast<uint32_t>(cap);
         hc::LaunchInfo li;
-        e = path == HC_PATH_STAGED ? hc::launch_staged(p, r->st[j], o.max_ctas, o.ctas_per_sm, &li)
-                                   : hc::launch_gather(p, r->st[j], o.max_ctas, o.ctas_per_sm, &li);
+        e = launch_search(path, p, r->st[j], o, &li);
         if (e == cudaSuccess)
             e = hc::launch_finish(sc.buf, p.out, p.cap, want_pos ? pos_out[i] : nullptr,
                                   want_pos ? static_cast<uint32_t>(std::min<size_t>(mo, windows)) : 0u,
-                                  r->hcounts_dev + i, r->st[j]);
+                                  p.n, r->hcounts_dev + i, r->st[j]);
         if (e != cudaSuccess) return cuda_fail(e, "batch launch");
         launches += 2;
     }

@@ -45,12 +45,15 @@ struct LaunchInfo {
 // Device-side entry points (hc_kernels.cu).  All enqueue on `st`.
 cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
+cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li);
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
 // One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,
 // ordering of <= kSmallSort positions into dst (first min(count, max_out), int64).
 cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
-                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st,
+                          uint32_t max_out, uint32_t n_bound, uint32_t *host_count_dev,
+                          cudaStream_t st,
                           unsigned long long *trace = nullptr);
 // Ordering of count > kSmallSort positions (CUB radix sort), first k written as int64.
 cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
@@ -60,9 +63,11 @@ constexpr uint32_t kSmallSort = 8192;
 int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
                       uint32_t slot_bytes, uint32_t nbox);
 int gather_smem_bytes(uint32_t alpha, uint32_t m);
+int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs);
 
 constexpr int kStagedThreads = 256;
 constexpr int kGatherThreads = 256;
+constexpr int kStreamThreads = 256;
 constexpr int kWarpBuf = 64;  // per-warp match buffer entries (shared memory)
 
 }  // namespace hc

@@ -32,6 +32,7 @@
 // Matches go to a per-warp shared buffer, flushed 32 at a time with one
 // atomicAdd (ballot/popc ranks); the host orders them afterwards.
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdio>
@@ -190,8 +191,8 @@ struct SmemText {
 struct FTable {
     uint32_t base;
     __device__ __forceinline__ uint32_t operator[](uint32_t v) const { return lds32(base + 4 * v); }
+    __device__ __forceinline__ bool pass(uint32_t v) const { return (*this)[v] != 0u; }   // l.6
 };
-
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
 // top Q bytes are meaningful.  Reads just the aligned 8-byte words holding y[p]
 // and y[p-Q+1] (both inside the text), so no byte outside [0, n) is touched.
@@ -539,9 +540,9 @@ __device__ __forceinline__ void run_survivors(const KParams &p, const T &txt, co
 // Phase A over lattice points [seg_lo, seg_hi), 32 * kUnroll per warp step: every
 // lane hashes the q-gram ending at its lattice point a_k = m-1 + k S (Fig. 5 l.4)
 // and tests F[v] != 0 (l.6).  Survivor segments are handed to `sink` (warp-uniform
-// call, ballot mask + the lane's k).  Full steps run without bounds checks.
-template <int Q, int SH, class T, class Sink>
-__device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, const FTable &sF,
+// call, ballot mask + the lane's window end a_k).  Full steps run without bounds checks.
+template <int Q, int SH, class T, class FT, class Sink>
+__device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, const FT &sF,
                                                uint32_t seg_lo, uint32_t seg_hi, uint32_t lane,
                                                Sink &&sink) {
     const uint32_t step = 32 * p.S;
@@ -555,22 +556,22 @@ __device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, c
         bool any = false;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            pass[u] = sF[qhash<Q, SH>(W[u], p.mask)] != 0u;
+            pass[u] = sF.pass(qhash<Q, SH>(W[u], p.mask));
             any |= pass[u];
         }
         if (__any_sync(HC_FULL, any)) {
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
                 const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
-                if (bm) sink(bm, pass[u], k0 + u * 32 + lane);
+                if (bm) sink(bm, pass[u], pos + u * step);
             }
         }
     }
     for (; k0 < seg_hi; k0 += 32, pos += step) {       // ragged tail, one round at a time
         const bool in = k0 + lane < seg_hi;
-        const bool pass = in && sF[qhash<Q, SH>(end8<Q>(txt, pos), p.mask)] != 0u;
+        const bool pass = in && sF.pass(qhash<Q, SH>(end8<Q>(txt, pos), p.mask));
         const uint32_t bm = __ballot_sync(HC_FULL, pass);
-        if (bm) sink(bm, pass, k0 + lane);
+        if (bm) sink(bm, pass, pos);
     }
 }
 
@@ -585,8 +586,7 @@ __device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, c
 // ~90% of the lattice survivors for one memory round trip per 32.
 template <int Q, int SH, class T>
 __device__ __forceinline__ bool first_steps_eval(const KParams &p, const T &txt, const FTable &sF,
-                                                 bool act, uint32_t k, uint32_t &start) {
-    const uint32_t e = p.m - 1 + k * p.S;
+                                                 bool act, uint32_t e, uint32_t &start) {
     start = e;
     if (!act) return false;
     if (p.m < 2 * Q) return true;                        // no walk step to test (R7)
@@ -612,14 +612,18 @@ struct WarpQueueSink {
     const T &txt;
     const FTable &sF;
     const uint8_t *sx;
-    uint32_t *q1, *q2;     // kWarpBuf entries each
+    uint32_t *q1, *q2;     // kWarpBuf entries each: lattice survivors' a_k / window ends
     uint32_t n1, n2;       // warp-uniform
     WarpOut &wo;
     uint32_t lane;
     __device__ __forceinline__ void steps(uint32_t c) {  // first steps of q1[0..c) -> q2
         const bool act = lane < c;
+        steps_e(act, act ? q1[lane] : 0u);
+    }
+    // first steps of the lattice survivor a_k = e of each active lane -> q2
+    __device__ __forceinline__ void steps_e(bool act, uint32_t e) {
         uint32_t start;
-        const bool keep = first_steps_eval<Q, SH>(p, txt, sF, act, act ? q1[lane] : 0u, start);
+        const bool keep = first_steps_eval<Q, SH>(p, txt, sF, act, e, start);
         const uint32_t bm = __ballot_sync(HC_FULL, keep);
         if (keep) q2[n2 + __popc(bm & lanemask_lt())] = start;
         n2 += __popc(bm);
@@ -634,8 +638,8 @@ struct WarpQueueSink {
             n2 = rest;
         }
     }
-    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
-        if (pass) q1[n1 + __popc(bm & lanemask_lt())] = k;
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t e) {
+        if (pass) q1[n1 + __popc(bm & lanemask_lt())] = e;
         n1 += __popc(bm);
         if (n1 >= 32) {
             __syncwarp();
@@ -675,7 +679,7 @@ struct RegionSink {
     const uint8_t *sx;
     uint32_t *region;   // kRegion entries (window ends)
     uint32_t cnt;       // warp-uniform
-    uint32_t *q1;       // kWarpBuf lattice survivors (k)
+    uint32_t *q1;       // kWarpBuf lattice survivors (a_k)
     uint32_t n1;        // warp-uniform
     WarpOut &wo;
     uint32_t lane;
@@ -698,9 +702,9 @@ struct RegionSink {
         const bool keep = first_steps_eval<Q, SH>(p, txt, sF, act, act ? q1[lane] : 0u, start);
         push(keep, start);
     }
-    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t k) {
+    __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t e) {
         if (p.debug == 3) return;                        // phase A only (measurement)
-        if (pass) q1[n1 + __popc(bm & lanemask_lt())] = k;
+        if (pass) q1[n1 + __popc(bm & lanemask_lt())] = e;
         n1 += __popc(bm);
         if (n1 >= 32) {
             __syncwarp();
@@ -1107,6 +1111,235 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     if (lane == 0) trace_cta(p, 1);   // last warp to get here wins
 }
 
+// ------------------------------------------------------------------ stream kernel
+// Small shifts (S <= 32), every text sector is read (f(m) = 1).  Each warp
+// owns a contiguous run of segments per chunk and stages exactly the chunk's lattice
+// q-gram bytes [k0 S + S - 1, k1 S + q - 2] into its own shared-memory buffer with
+// 16-byte cp.async copies (coalesced, L2-only), kStreamBufs - 1 chunks ahead of the
+// one it filters: no CTA-wide barrier, no hand-off between warps.  Phase A reads the
+// buffer; the lattice survivors go through first_steps and phase B on global text
+// (the chunk was just streamed through L2), exactly as on the gather path.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr uint32_t kStreamQ1 = 32 * (kUnroll + 1);   // lattice survivor queue per warp
+struct StreamLayout {
+    uint32_t f_off, x_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
+};
+__host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m, uint32_t nwarps,
+                                                      uint32_t buf_bytes, uint32_t bufs) {
+    StreamLayout L;
+    L.f_off = 0;
+    L.x_off = round_up((1u << alpha) * 4u, 16);
+    L.q_off = L.x_off + round_up(m + 8, 16);
+    L.q2_off = L.q_off + nwarps * kStreamQ1 * 4u;
+    L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
+    L.ctr_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    L.buf_off = round_up(L.ctr_off + nwarps * 4u + 16, 128);
+    L.total = L.buf_off + nwarps * bufs * buf_bytes;
+    return L;
+}
+int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs) {
+    return static_cast<int>(stream_layout(alpha, m, kStreamThreads / 32, buf_bytes, bufs).total);
+}
+
+// Text bytes of chunk c: the q-grams ending at a_k, k in [k0, k1).
+struct StreamChunk {
+    uint32_t k0, k1, first, last;   // bytes [first, last] of y
+};
+__device__ __forceinline__ StreamChunk stream_chunk(const KParams &p, uint32_t c) {
+    StreamChunk g;
+    g.k0 = c * p.seg_per_chunk;
+    g.k1 = min(g.k0 + p.seg_per_chunk, p.K);
+    g.first = g.k0 * p.S + p.S - 1;                 // a_k0 - q + 1
+    g.last = p.m - 1 + (g.k1 - 1) * p.S;            // a_{k1-1}
+    return g;
+}
+// Issues chunk c's copies into the buffer at shared address `buf` (one warp).  The
+// 16-byte words wholly inside y are copied with cp.async; the bytes of the partial
+// words at the two ends of an unaligned text are stored directly (first/last chunk).
+__device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint32_t buf,
+                                             uint32_t lane) {
+    if (c < p.nchunks) {
+        const StreamChunk g = stream_chunk(p, c);
+        const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
+        const uintptr_t A = (y + g.first) & ~static_cast<uintptr_t>(15);
+        const uint32_t nbytes =
+            static_cast<uint32_t>(((y + g.last + 16) & ~static_cast<uintptr_t>(15)) - A);
+        const uintptr_t ye = y + p.n;
+        if (A >= y && A + nbytes <= ye) {               // warp-uniform: interior chunk
+            const uint8_t *src = reinterpret_cast<const uint8_t *>(A);
+            for (uint32_t o = 16 * lane; o < nbytes; o += 16 * 32) cp_async16(buf + o, src + o);
+        } else {
+            for (uint32_t o = 16 * lane; o < nbytes; o += 16 * 32) {
+                const uintptr_t a = A + o;
+                if (a >= y && a + 16 <= ye) {
+                    cp_async16(buf + o, reinterpret_cast<const void *>(a));
+                } else {
+                    for (uint32_t b = 0; b < 16; ++b)
+                        if (a + b >= y && a + b < ye)
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + o + b),
+                                         "r"(static_cast<uint32_t>(
+                                             __ldg(reinterpret_cast<const uint8_t *>(a + b))))
+                                         : "memory");
+                }
+            }
+        }
+    }
+    cp_async_commit();   // one group per issue (possibly empty) keeps the count uniform
+}
+
+// Phase A of the stream path over lattice points [k0, k1) of a staged chunk: the same
+// l.4-6 test as filter_lattice, but the survivors are appended to a per-warp queue
+// (q1, count n1, shared slot counter ctr) with one shared atomic per lane that has
+// any, and the queue is drained (first_steps, phase B: calls) only between runs of
+// trips, so the trip loop has no call in it and keeps its state in registers.
+template <int Q, int SH>
+struct StreamQueue {
+    uint32_t *q1;     // kStreamQ1 window ends a_k
+    uint32_t *ctr;    // shared slot counter (= n1 between trips)
+    uint32_t n1;      // warp-uniform count
+    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText> &sink, uint32_t lane) {
+        __syncwarp();
+        const uint32_t e = q1[n1 - 32 + lane];
+        n1 -= 32;
+        __syncwarp();
+        if (lane == 0) *ctr = n1;
+        __syncwarp();
+        sink.steps_e(true, e);
+    }
+    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText> &sink, uint32_t lane) {
+        while (n1 >= 32) drain32(sink, lane);
+        if (n1) {
+            __syncwarp();
+            const bool act = lane < n1;
+            const uint32_t e = act ? q1[lane] : 0u;
+            n1 = 0;
+            __syncwarp();
+            if (lane == 0) *ctr = 0;
+            __syncwarp();
+            sink.steps_e(act, e);
+        }
+    }
+};
+
+template <int Q, int SH>
+__device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &txt, const FTable &sF,
+                                              uint32_t k0, uint32_t k1, uint32_t lane,
+                                              StreamQueue<Q, SH> &qu,
+                                              WarpQueueSink<Q, SH, GlobalText> &sink) {
+    const uint32_t step = 32 * p.S;
+    uint32_t pos = p.m - 1 + (k0 + lane) * p.S;   // window end a_k of lattice point k0 + lane
+    uint32_t k = k0;
+    while (true) {
+        while (k + 32 * kUnroll <= k1 && qu.n1 < 32) {
+            uint64_t W[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
+            uint32_t pm = 0;
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
+            const uint32_t c = __popc(pm);
+            const uint32_t tot = __reduce_add_sync(HC_FULL, c);
+            if (tot) {
+                if (c) {
+                    uint32_t slot = atomicAdd(qu.ctr, c);
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u)
+                        if ((pm >> u) & 1u) qu.q1[slot++] = pos + u * step;
+                }
+                qu.n1 += tot;
+            }
+            k += 32 * kUnroll;
+            pos += kUnroll * step;
+        }
+        if (qu.n1 < 32) break;
+        qu.drain32(sink, lane);
+    }
+    for (; k < k1; k += 32, pos += step) {          // ragged tail, one round at a time
+        const bool in = k + lane < k1;
+        const bool pass = in && sF.pass(qhash<Q, SH>(end8<Q>(txt, pos), p.mask));
+        const uint32_t bm = __ballot_sync(HC_FULL, pass);
+        if (bm) {
+            if (pass) qu.q1[qu.n1 + __popc(bm & lanemask_lt())] = pos;
+            qu.n1 += __popc(bm);
+            __syncwarp();
+            if (lane == 0) *qu.ctr = qu.n1;
+            if (qu.n1 >= 32) qu.drain32(sink, lane);
+        }
+    }
+}
+
+template <int Q, int SH, int NB>
+__device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
+                                            WarpQueueSink<Q, SH, GlobalText> &sink,
+                                            StreamQueue<Q, SH> &qu, uint32_t bufs0,
+                                            uint32_t gw, uint32_t total_warps, uint32_t lane) {
+    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
+#pragma unroll
+    for (int b = 0; b < NB - 1; ++b) stream_issue(p, gw + b * total_warps, bufs0 + b * p.stage_bytes, lane);
+    uint32_t b = 0;
+    for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
+        // refill the buffer filtered last round with the chunk NB-1 ahead
+        const uint32_t bn = b == 0 ? NB - 1 : b - 1;
+        stream_issue(p, c + (NB - 1) * total_warps, bufs0 + bn * p.stage_bytes, lane);
+        cp_async_wait<NB - 1>();   // chunk c's group is complete (this lane's copies)
+        __syncwarp();              // ... and every lane's, visible to the warp
+        const StreamChunk g = stream_chunk(p, c);
+        const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
+        const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
+        stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+        __syncwarp();              // every lane is done with buffer b before its refill
+        b = b + 1 == NB ? 0 : b + 1;
+    }
+    cp_async_wait<0>();
+    qu.drain_all(sink, lane);
+}
+
+template <int Q, int SH>
+__global__ void __launch_bounds__(kStreamThreads) stream_kernel(const KParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t NW = kStreamThreads / 32;
+    const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages);
+    uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
+    uint8_t *sx = smem + L.x_off;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) trace_cta(p, 0);
+    pdl_launch_dependents();
+    const uint32_t total_warps = gridDim.x * NW;
+    const uint32_t gw = blockIdx.x * NW + warp;
+    const uint32_t bufs0 = smem_u32(smem + L.buf_off) + warp * p.stages * p.stage_bytes;
+    load_table(p, sFp, sx);
+    if (tid == 0) s_params = p;
+    __syncthreads();
+    const FTable sF{fence_value(smem_u32(sFp))};
+    WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
+    const GlobalText gtxt{p.y};
+    WarpQueueSink<Q, SH, GlobalText> sink{p, gtxt, sF, sx, nullptr,
+                                          reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
+                                          0u, 0u, wo, lane};
+    uint32_t *ctr = reinterpret_cast<uint32_t *>(smem + L.ctr_off) + warp;
+    if (lane == 0) *ctr = 0;
+    __syncwarp();
+    StreamQueue<Q, SH> qu{reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kStreamQ1, ctr, 0u};
+    if (p.stages == 2)
+        stream_loop<Q, SH, 2>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    else if (p.stages == 3)
+        stream_loop<Q, SH, 3>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    else
+        stream_loop<Q, SH, 4>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    sink.drain();
+    wo.flush(p, lane);
+    if (lane == 0) trace_cta(p, 1);
+}
+
 // ------------------------------------------------------------------ launchers
 using KernFn = void (*)(const KParams);
 
@@ -1130,6 +1363,10 @@ static KernFn pick(uint32_t q, uint32_t s) {
 template <int Q, int SH>
 struct PickStaged {
     static KernFn fn() { return staged_kernel<Q, SH>; }
+};
+template <int Q, int SH>
+struct PickStream {
+    static KernFn fn() { return stream_kernel<Q, SH>; }
 };
 template <int Q, int SH>
 struct PickGather {
@@ -1221,6 +1458,15 @@ cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int c
     return launch_common(kern, p, kGatherThreads, smem, ctas, max_ctas, ctas_per_sm, st, li);
 }
 
+cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li) {
+    KernFn kern = pick<PickStream>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
+    const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages);
+    const int ctas = static_cast<int>((p.nchunks + kStreamThreads / 32 - 1) / (kStreamThreads / 32));
+    return launch_common(kern, p, kStreamThreads, smem, ctas, max_ctas, ctas_per_sm, st, li);
+}
+
 // ------------------------------------------------------------------ ordering
 __global__ void widen_kernel(const uint32_t *src, int64_t *dst, uint32_t k) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
@@ -1230,14 +1476,23 @@ __global__ void widen_kernel(const uint32_t *src, int64_t *dst, uint32_t k) {
 
 // Runs right after the search kernel, one CTA: publishes the count to the host
 // (mapped pinned word), resets the device counter for the next call, and when
-// 1 <= count <= kSmallSort orders the positions in shared memory (bitonic sort of
-// distinct keys) and writes the first min(count, max_out) as int64.
-__global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const uint32_t *pos,
-                                                      uint32_t cap, int64_t *dst,
-                                                      uint32_t max_out,
-                                                      volatile uint32_t *host_count,
-                                                      unsigned long long *trace) {
-    __shared__ uint32_t s[kSmallSort];
+// 1 <= count <= kSmallSort orders the positions (distinct keys) and writes the first
+// min(count, max_out) as int64.  Up to kRankSort keys are ordered by rank counting
+// (key i goes to #{j : key_j < key_i}); larger sets by a block radix sort over the
+// ceil(log2 n) significant bits, keys in registers (8 per thread).
+constexpr uint32_t kRankSort = 256;
+constexpr int kFinishThreads = 1024;
+constexpr int kFinishItems = kSmallSort / kFinishThreads;
+using FinishSort = cub::BlockRadixSort<uint32_t, kFinishThreads, kFinishItems>;
+__global__ void __launch_bounds__(kFinishThreads) finish_kernel(uint32_t *counter, const uint32_t *pos,
+                                                                uint32_t cap, int64_t *dst,
+                                                                uint32_t max_out, uint32_t nbits,
+                                                                volatile uint32_t *host_count,
+                                                                unsigned long long *trace) {
+    __shared__ union {
+        typename FinishSort::TempStorage sort;
+        uint32_t keys[kRankSort];
+    } sm;
     if (trace && threadIdx.x == 0) trace[0] = gtimer();
     pdl_wait();   // the search grid has completed and its writes are visible
     if (trace && threadIdx.x == 0) trace[1] = gtimer();
@@ -1250,39 +1505,47 @@ __global__ void __launch_bounds__(1024) finish_kernel(uint32_t *counter, const u
     }
     if (dst == nullptr || max_out == 0 || count == 0 || count > cap || count > kSmallSort) return;
     const uint32_t k = min(count, max_out);
+    const uint32_t t = threadIdx.x;
     if (count == 1) {
-        if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(pos[0]);
+        if (t == 0) dst[0] = static_cast<int64_t>(pos[0]);
         return;
     }
-    uint32_t P = 1;
-    while (P < count) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < count ? pos[i] : 0xffffffffu;
-    __syncthreads();
-    for (uint32_t size = 2; size <= P; size <<= 1) {
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                const uint32_t pr = i ^ stride;
-                if (pr > i) {
-                    const bool asc = (i & size) == 0;
-                    const uint32_t a = s[i], b = s[pr];
-                    if ((a > b) == asc) {
-                        s[i] = b;
-                        s[pr] = a;
-                    }
-                }
-            }
-            __syncthreads();
+    if (count <= kRankSort) {
+        if (t < count) sm.keys[t] = pos[t];
+        __syncthreads();
+        if (t < count) {
+            const uint32_t key = sm.keys[t];
+            uint32_t r = 0;
+            for (uint32_t i = 0; i < count; ++i) r += sm.keys[i] < key;
+            if (r < k) dst[r] = static_cast<int64_t>(key);
         }
+        return;
     }
-    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) dst[i] = static_cast<int64_t>(s[i]);
+    uint32_t keys[kFinishItems];
+#pragma unroll
+    for (int i = 0; i < kFinishItems; ++i) {
+        const uint32_t g = t * kFinishItems + i;   // blocked arrangement
+        keys[i] = g < count ? pos[g] : 0xffffffffu;
+    }
+    // real keys are < 2^nbits, the all-ones pads have bit nbits set: sorting bits
+    // [0, nbits] puts the pads last
+    const uint32_t hi = nbits < 32 ? nbits + 1 : 32;
+    FinishSort(sm.sort).SortBlockedToStriped(keys, 0, static_cast<int>(hi));
+#pragma unroll
+    for (int i = 0; i < kFinishItems; ++i) {
+        const uint32_t r = t + i * kFinishThreads;  // striped: rank r
+        if (r < k) dst[r] = static_cast<int64_t>(keys[i]);
+    }
 }
 
 cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
-                          uint32_t max_out, uint32_t *host_count_dev, cudaStream_t st,
-                          unsigned long long *trace) {
+                          uint32_t max_out, uint32_t n_bound, uint32_t *host_count_dev,
+                          cudaStream_t st, unsigned long long *trace) {
+    uint32_t nbits = 1;
+    while (nbits < 32 && (static_cast<uint64_t>(1) << nbits) <= n_bound) ++nbits;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(1024);
+    cfg.blockDim = dim3(kFinishThreads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1290,7 +1553,7 @@ cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, finish_kernel, counter, pos, cap, dst, max_out,
+    return cudaLaunchKernelEx(&cfg, finish_kernel, counter, pos, cap, dst, max_out, nbits,
                               host_count_dev, trace);
 }
 
