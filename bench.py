@@ -503,8 +503,8 @@ def main():
                         d2h += 8 + 8 * c
                     for h in hs:
                         h.close()
+                    torch.cuda.synchronize(dev)   # this m's positions are on the host
                     if os.environ.get("HC_BENCH_DEBUG"):
-                        torch.cuda.synchronize(dev)
                         print(f"e2e m={m}: {1e3 * (time.perf_counter() - t_m):.2f} ms", file=sys.stderr)
                 continue
             for (m, q, a, o, x), c in zip(work, counts):

@@ -111,6 +111,7 @@ typedef struct hc_search_opts {
                                   %globaltimer stamps per (CTA, tile), or NULL */
     int trace_tiles;
     int surv_warps;   /* staged: survivor/producer warps per CTA (0 = default) */
+    int block_warps;  /* stream: warps per CTA, 1..8 (0 = default 8) */
 } hc_search_opts;
 
 typedef struct hc_search_stats {

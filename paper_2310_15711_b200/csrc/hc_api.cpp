@@ -173,6 +173,7 @@ constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
 constexpr uint32_t kDefaultSegPerLane = 2;
 constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per warp chunk
 constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
+constexpr uint32_t kDefaultStreamWarps = 8;     // stream path: warps per CTA
 
 cudaError_t launch_search(int path, const hc::KParams &p, cudaStream_t st, const hc_search_opts &o,
                           hc::LaunchInfo *li) {
@@ -247,12 +248,15 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         const uint32_t unit = S <= 32 ? 128u : 32u;
         p.seg_per_chunk = unit * std::max<uint32_t>(1u, (target / S + unit / 2) / unit);
         p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
-        // chunk bytes [k0 S + S - 1, k1 S + q - 2] plus 16-byte alignment slack
-        p.stage_bytes = (p.seg_per_chunk * S + q + 32 + 15) & ~15u;
+        // chunk bytes [a_k0 - 2q + 1, a_k1 - q] plus 16-byte alignment slack
+        p.stage_bytes = (p.seg_per_chunk * S + 2 * q + 32 + 15) & ~15u;
         p.stages = o.stages >= 2 && o.stages <= 4 ? static_cast<uint32_t>(o.stages) : kDefaultStreamBufs;
+        p.block_warps = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps)
+                                                                  : kDefaultStreamWarps;
         // shifts too long for per-warp buffers (S > ~200) take the gather path, which
         // reads only the q-grams it hashes anyway
-        if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages) > max_smem_optin(h->device))
+        if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps) >
+            max_smem_optin(h->device))
             path = HC_PATH_GATHER;
     }
     if (path == HC_PATH_GATHER) {

@@ -28,6 +28,7 @@ struct KParams {
     // gather path
     uint32_t seg_per_chunk; // segments per warp chunk
     uint32_t nchunks;
+    uint32_t block_warps;   // stream path: warps per CTA
     // output
     uint32_t *out;       // positions (window starts), unordered; NULL = count only
     uint32_t cap;        // capacity of out
@@ -63,11 +64,11 @@ constexpr uint32_t kSmallSort = 8192;
 int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
                       uint32_t slot_bytes, uint32_t nbox);
 int gather_smem_bytes(uint32_t alpha, uint32_t m);
-int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs);
+int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs, uint32_t nwarps);
 
 constexpr int kStagedThreads = 256;
 constexpr int kGatherThreads = 256;
-constexpr int kStreamThreads = 256;
+constexpr int kStreamMaxThreads = 256;
 constexpr int kWarpBuf = 64;  // per-warp match buffer entries (shared memory)
 
 }  // namespace hc

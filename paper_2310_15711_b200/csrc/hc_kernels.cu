@@ -621,9 +621,12 @@ struct WarpQueueSink {
         steps_e(act, act ? q1[lane] : 0u);
     }
     // first steps of the lattice survivor a_k = e of each active lane -> q2
-    __device__ __forceinline__ void steps_e(bool act, uint32_t e) {
+    __device__ __forceinline__ void steps_e(bool act, uint32_t e) { steps_e_on(txt, act, e); }
+    // the same, reading the first steps' q-grams from `t2` (e.g. a shared-memory stage)
+    template <class T2>
+    __device__ __forceinline__ void steps_e_on(const T2 &t2, bool act, uint32_t e) {
         uint32_t start;
-        const bool keep = first_steps_eval<Q, SH>(p, txt, sF, act, e, start);
+        const bool keep = first_steps_eval<Q, SH>(p, t2, sF, act, e, start);
         const uint32_t bm = __ballot_sync(HC_FULL, keep);
         if (keep) q2[n2 + __popc(bm & lanemask_lt())] = start;
         n2 += __popc(bm);
@@ -1145,11 +1148,13 @@ __host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m
     L.total = L.buf_off + nwarps * bufs * buf_bytes;
     return L;
 }
-int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs) {
-    return static_cast<int>(stream_layout(alpha, m, kStreamThreads / 32, buf_bytes, bufs).total);
+int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs,
+                      uint32_t nwarps) {
+    return static_cast<int>(stream_layout(alpha, m, nwarps, buf_bytes, bufs).total);
 }
 
-// Text bytes of chunk c: the q-grams ending at a_k, k in [k0, k1).
+// Text bytes of chunk c: the q-grams ending at a_k, k in [k0, k1), and at a_k - q and
+// a_k - q + S (the first steps of Fig. 5 for a lattice survivor).
 struct StreamChunk {
     uint32_t k0, k1, first, last;   // bytes [first, last] of y
 };
@@ -1157,8 +1162,12 @@ __device__ __forceinline__ StreamChunk stream_chunk(const KParams &p, uint32_t c
     StreamChunk g;
     g.k0 = c * p.seg_per_chunk;
     g.k1 = min(g.k0 + p.seg_per_chunk, p.K);
-    g.first = g.k0 * p.S + p.S - 1;                 // a_k0 - q + 1
-    g.last = p.m - 1 + (g.k1 - 1) * p.S;            // a_{k1-1}
+    // bytes [a_k0 - 2q + 1, a_{k1} - q]: the lattice q-grams plus those of the first
+    // steps (first_steps_eval reads the q-grams ending at a_k - q and a_k - q + S)
+    const uint32_t a0 = p.m - 1 + g.k0 * p.S;
+    g.first = a0 + 1 >= 2 * p.q ? a0 + 1 - 2 * p.q : 0u;
+    const uint32_t alast = p.m - 1 + (g.k1 - 1) * p.S;
+    g.last = max(alast, min(alast + p.S - p.q, p.n - 1));
     return g;
 }
 // Issues chunk c's copies into the buffer at shared address `buf` (one warp).  The
@@ -1205,17 +1214,21 @@ struct StreamQueue {
     uint32_t *q1;     // kStreamQ1 window ends a_k
     uint32_t *ctr;    // shared slot counter (= n1 between trips)
     uint32_t n1;      // warp-uniform count
-    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText> &sink, uint32_t lane) {
+    // first steps of 32 queued survivors, on the chunk's stage (the queue only ever
+    // holds survivors of the chunk being filtered: it is drained at the chunk's end)
+    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText> &sink,
+                                            const SmemText &txt, uint32_t lane) {
         __syncwarp();
         const uint32_t e = q1[n1 - 32 + lane];
         n1 -= 32;
         __syncwarp();
         if (lane == 0) *ctr = n1;
         __syncwarp();
-        sink.steps_e(true, e);
+        sink.steps_e_on(txt, true, e);
     }
-    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText> &sink, uint32_t lane) {
-        while (n1 >= 32) drain32(sink, lane);
+    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText> &sink,
+                                              const SmemText &txt, uint32_t lane) {
+        while (n1 >= 32) drain32(sink, txt, lane);
         if (n1) {
             __syncwarp();
             const bool act = lane < n1;
@@ -1224,7 +1237,7 @@ struct StreamQueue {
             __syncwarp();
             if (lane == 0) *ctr = 0;
             __syncwarp();
-            sink.steps_e(act, e);
+            sink.steps_e_on(txt, act, e);
         }
     }
 };
@@ -1246,6 +1259,7 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
                 pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
+            if (p.debug == 3) pm = 0;                   // phase A alone (measurement)
             const uint32_t c = __popc(pm);
             const uint32_t tot = __reduce_add_sync(HC_FULL, c);
             if (tot) {
@@ -1261,7 +1275,7 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             pos += kUnroll * step;
         }
         if (qu.n1 < 32) break;
-        qu.drain32(sink, lane);
+        qu.drain32(sink, txt, lane);
     }
     for (; k < k1; k += 32, pos += step) {          // ragged tail, one round at a time
         const bool in = k + lane < k1;
@@ -1272,7 +1286,7 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             qu.n1 += __popc(bm);
             __syncwarp();
             if (lane == 0) *qu.ctr = qu.n1;
-            if (qu.n1 >= 32) qu.drain32(sink, lane);
+            if (qu.n1 >= 32) qu.drain32(sink, txt, lane);
         }
     }
 }
@@ -1295,18 +1309,20 @@ __device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
         const StreamChunk g = stream_chunk(p, c);
         const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
         const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
-        stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+        if (p.debug != 1) {
+            stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+            qu.drain_all(sink, txt, lane);
+        }
         __syncwarp();              // every lane is done with buffer b before its refill
         b = b + 1 == NB ? 0 : b + 1;
     }
     cp_async_wait<0>();
-    qu.drain_all(sink, lane);
 }
 
 template <int Q, int SH>
-__global__ void __launch_bounds__(kStreamThreads) stream_kernel(const KParams p) {
+__global__ void __launch_bounds__(kStreamMaxThreads) stream_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr uint32_t NW = kStreamThreads / 32;
+    const uint32_t NW = blockDim.x / 32;
     const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages);
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
@@ -1462,9 +1478,10 @@ cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int c
                           LaunchInfo *li) {
     KernFn kern = pick<PickStream>(p.q, p.s);
     if (!kern) return cudaErrorInvalidValue;
-    const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages);
-    const int ctas = static_cast<int>((p.nchunks + kStreamThreads / 32 - 1) / (kStreamThreads / 32));
-    return launch_common(kern, p, kStreamThreads, smem, ctas, max_ctas, ctas_per_sm, st, li);
+    const uint32_t nw = p.block_warps;
+    const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, nw);
+    const int ctas = static_cast<int>((p.nchunks + nw - 1) / nw);
+    return launch_common(kern, p, static_cast<int>(32 * nw), smem, ctas, max_ctas, ctas_per_sm, st, li);
 }
 
 // ------------------------------------------------------------------ ordering

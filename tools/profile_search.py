@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--absent", action="store_true", help="random pattern (likely absent)")
     ap.add_argument("--trace", type=int, default=0, help="trace N tiles per CTA (staged)")
     ap.add_argument("--sw", type=int, default=0, help="survivor warps (staged)")
+    ap.add_argument("--bw", type=int, default=0, help="warps per CTA (stream)")
     ap.add_argument("--noflush", action="store_true", help="no L2 flush between calls")
     args = ap.parse_args()
     cfg = I.CONFIGS[args.config]
@@ -87,7 +88,7 @@ def main():
                                 stages=args.stages, seg_per_lane=args.spl, time_kernel=1,
                                 ctas_per_sm=args.cps, debug=args.debug,
                                 tma_chunk=args.chunk, trace=tr.data_ptr() if args.trace else 0,
-                                trace_tiles=args.trace, surv_warps=args.sw)
+                                trace_tiles=args.trace, surv_warps=args.sw, block_warps=args.bw)
             torch.cuda.synchronize()
             print(f"m={m} q={q} a={a} rep={r} count={len(res)} kernel_us={st['kernel_ms']*1e3:.1f} "
                   f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}"

@@ -7,8 +7,8 @@ timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpur
 python bench.py --steps 1 --warmup 3 --per-m 5 --no-e2e --no-cpu > gpurun_out/bench_small.json 2> gpurun_out/bench_small.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 3 --per-m 5 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
-# full capture of the staged kernel (m=8, m=16) and the gather kernel (m=128)
-python tools/profile_search.py --m 8 16 128 --reps 1 > gpurun_out/pf_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"staged|gather" -c 3 \
-    -o gpurun_out/prof_round python tools/profile_search.py --m 8 16 128 --reps 1 > gpurun_out/ncu_full.log 2>&1
+# full capture of the stream kernel (m=8, m=16, m=32) and the gather kernel (m=128)
+python tools/profile_search.py --m 8 16 32 128 --reps 1 > gpurun_out/pf_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"stream_kernel|gather_kernel" -c 4 \
+    -o gpurun_out/prof_round python tools/profile_search.py --m 8 16 32 128 --reps 1 > gpurun_out/ncu_full.log 2>&1
 echo done

@@ -1,3 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.txt 2>&1
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
-timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+for spl in 1 2 4 8; do
+  echo "== gather spl=$spl"
+  python tools/profile_search.py --m 64 128 256 512 1024 --reps 3 --path 2 --spl $spl 2>&1 | grep -v "rep=0" | awk '{print $1, $5, $6, $7}'
+done > gpurun_out/exp.txt 2>&1
