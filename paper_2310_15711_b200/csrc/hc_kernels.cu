@@ -1131,7 +1131,11 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr uint32_t kStreamQ1 = 32 * (kUnroll + 1);   // lattice survivor queue per warp
+#ifndef HC_STREAM_UNROLL
+#define HC_STREAM_UNROLL 4
+#endif
+constexpr int kStreamUnroll = HC_STREAM_UNROLL;        // stream: lattice rounds per trip
+constexpr uint32_t kStreamQ1 = 32 * (kStreamUnroll + 1);   // lattice survivor queue per warp
 struct StreamLayout {
     uint32_t f_off, x_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
 };
@@ -1251,13 +1255,13 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
     uint32_t pos = p.m - 1 + (k0 + lane) * p.S;   // window end a_k of lattice point k0 + lane
     uint32_t k = k0;
     while (true) {
-        while (k + 32 * kUnroll <= k1 && qu.n1 < 32) {
-            uint64_t W[kUnroll];
+        while (k + 32 * kStreamUnroll <= k1 && qu.n1 < 32) {
+            uint64_t W[kStreamUnroll];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
+            for (int u = 0; u < kStreamUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
             uint32_t pm = 0;
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
+            for (int u = 0; u < kStreamUnroll; ++u)
                 pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
             if (p.debug == 3) pm = 0;                   // phase A alone (measurement)
             const uint32_t c = __popc(pm);
@@ -1266,13 +1270,13 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
                 if (c) {
                     uint32_t slot = atomicAdd(qu.ctr, c);
 #pragma unroll
-                    for (int u = 0; u < kUnroll; ++u)
+                    for (int u = 0; u < kStreamUnroll; ++u)
                         if ((pm >> u) & 1u) qu.q1[slot++] = pos + u * step;
                 }
                 qu.n1 += tot;
             }
-            k += 32 * kUnroll;
-            pos += kUnroll * step;
+            k += 32 * kStreamUnroll;
+            pos += kStreamUnroll * step;
         }
         if (qu.n1 < 32) break;
         qu.drain32(sink, txt, lane);
@@ -1494,12 +1498,18 @@ __global__ void widen_kernel(const uint32_t *src, int64_t *dst, uint32_t k) {
 // Runs right after the search kernel, one CTA: publishes the count to the host
 // (mapped pinned word), resets the device counter for the next call, and when
 // 1 <= count <= kSmallSort orders the positions (distinct keys) and writes the first
-// min(count, max_out) as int64.  Up to kRankSort keys are ordered by rank counting
-// (key i goes to #{j : key_j < key_i}); larger sets by a block radix sort over the
-// ceil(log2 n) significant bits, keys in registers (8 per thread).
+// min(count, max_out) as int64:
+//   count <= kRankSort : rank counting (key i goes to #{j : key_j < key_i});
+//   otherwise          : a bucket pass on the top 11 of the ceil(log2 n) bits
+//                        (shared counters, scan, scatter), then each key's rank inside
+//                        its bucket by counting; a bucket larger than kBucketMax
+//                        (skewed positions) sends the whole set to a block radix sort.
 constexpr uint32_t kRankSort = 256;
 constexpr int kFinishThreads = 1024;
 constexpr int kFinishItems = kSmallSort / kFinishThreads;
+constexpr uint32_t kBucketBits = 11;
+constexpr uint32_t kBuckets = 1u << kBucketBits;
+constexpr uint32_t kBucketMax = 32;
 using FinishSort = cub::BlockRadixSort<uint32_t, kFinishThreads, kFinishItems>;
 __global__ void __launch_bounds__(kFinishThreads) finish_kernel(uint32_t *counter, const uint32_t *pos,
                                                                 uint32_t cap, int64_t *dst,
@@ -1508,7 +1518,12 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(uint32_t *counte
                                                                 unsigned long long *trace) {
     __shared__ union {
         typename FinishSort::TempStorage sort;
-        uint32_t keys[kRankSort];
+        struct {
+            uint32_t cnt[kBuckets];     // keys per bucket, then bucket starts
+            uint32_t keys[kSmallSort];  // keys grouped by bucket
+            uint32_t warp_sum[32];
+            uint32_t maxcnt;
+        } b;
     } sm;
     if (trace && threadIdx.x == 0) trace[0] = gtimer();
     pdl_wait();   // the search grid has completed and its writes are visible
@@ -1522,32 +1537,91 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(uint32_t *counte
     }
     if (dst == nullptr || max_out == 0 || count == 0 || count > cap || count > kSmallSort) return;
     const uint32_t k = min(count, max_out);
-    const uint32_t t = threadIdx.x;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (count == 1) {
         if (t == 0) dst[0] = static_cast<int64_t>(pos[0]);
         return;
     }
     if (count <= kRankSort) {
-        if (t < count) sm.keys[t] = pos[t];
+        if (t < count) sm.b.keys[t] = pos[t];
         __syncthreads();
         if (t < count) {
-            const uint32_t key = sm.keys[t];
+            const uint32_t key = sm.b.keys[t];
             uint32_t r = 0;
-            for (uint32_t i = 0; i < count; ++i) r += sm.keys[i] < key;
+            for (uint32_t i = 0; i < count; ++i) r += sm.b.keys[i] < key;
             if (r < k) dst[r] = static_cast<int64_t>(key);
         }
         return;
     }
+    // bucket pass: key -> bucket key >> shift (< kBuckets since key < 2^nbits)
+    const uint32_t shift = nbits > kBucketBits ? nbits - kBucketBits : 0u;
+    for (uint32_t i = t; i < kBuckets; i += kFinishThreads) sm.b.cnt[i] = 0;
+    if (t == 0) sm.b.maxcnt = 0;
+    __syncthreads();
+    uint32_t key[kFinishItems], slot[kFinishItems];
+#pragma unroll
+    for (int i = 0; i < kFinishItems; ++i) {
+        const uint32_t g = t + i * kFinishThreads;
+        key[i] = g < count ? pos[g] : 0u;
+        slot[i] = g < count ? atomicAdd(&sm.b.cnt[key[i] >> shift], 1u) : 0u;
+    }
+    __syncthreads();
+    // exclusive scan of the 2048 counters: 2 per thread, warp shuffles, warp totals
+    const uint32_t c0 = sm.b.cnt[2 * t], c1 = sm.b.cnt[2 * t + 1];
+    uint32_t incl = c0 + c1;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(HC_FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) sm.b.warp_sum[warp] = incl;
+    const uint32_t mx = __reduce_max_sync(HC_FULL, max(c0, c1));
+    if (lane == 0) atomicMax(&sm.b.maxcnt, mx);
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = sm.b.warp_sum[lane];
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(HC_FULL, w, o);
+            if (lane >= o) w += v;
+        }
+        sm.b.warp_sum[lane] = w - sm.b.warp_sum[lane];   // exclusive warp offsets
+    }
+    __syncthreads();
+    const uint32_t base = sm.b.warp_sum[warp] + incl - (c0 + c1);
+    const bool skewed = sm.b.maxcnt > kBucketMax;
+    __syncthreads();
+    if (!skewed) {
+        sm.b.cnt[2 * t] = base;              // bucket starts
+        sm.b.cnt[2 * t + 1] = base + c0;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kFinishItems; ++i)
+            if (t + i * kFinishThreads < count) sm.b.keys[sm.b.cnt[key[i] >> shift] + slot[i]] = key[i];
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kFinishItems; ++i) {
+            if (t + i * kFinishThreads >= count) continue;
+            const uint32_t bk = key[i] >> shift;
+            const uint32_t lo = sm.b.cnt[bk];
+            const uint32_t hi = bk + 1 < kBuckets ? sm.b.cnt[bk + 1] : count;
+            uint32_t r = lo;
+            for (uint32_t j = lo; j < hi; ++j) r += sm.b.keys[j] < key[i];
+            if (r < k) dst[r] = static_cast<int64_t>(key[i]);
+        }
+        return;
+    }
+    // skewed positions: block radix sort (blocked arrangement, all-ones pads)
     uint32_t keys[kFinishItems];
 #pragma unroll
     for (int i = 0; i < kFinishItems; ++i) {
-        const uint32_t g = t * kFinishItems + i;   // blocked arrangement
+        const uint32_t g = t * kFinishItems + i;
         keys[i] = g < count ? pos[g] : 0xffffffffu;
     }
     // real keys are < 2^nbits, the all-ones pads have bit nbits set: sorting bits
     // [0, nbits] puts the pads last
-    const uint32_t hi = nbits < 32 ? nbits + 1 : 32;
-    FinishSort(sm.sort).SortBlockedToStriped(keys, 0, static_cast<int>(hi));
+    const uint32_t hb = nbits < 32 ? nbits + 1 : 32;
+    FinishSort(sm.sort).SortBlockedToStriped(keys, 0, static_cast<int>(hb));
 #pragma unroll
     for (int i = 0; i < kFinishItems; ++i) {
         const uint32_t r = t + i * kFinishThreads;  // striped: rank r

@@ -265,3 +265,27 @@ def test_search_batch_matches_single_searches():
     assert st["kernel_ms"] > 0
     cnts = hc.search_batch_raw(hs, yd.data_ptr(), yd.numel(), None, None, 0)
     assert cnts == [len(w) for w in want]
+
+
+@pytest.mark.parametrize("path", [hc.PATH_STREAM, hc.PATH_GATHER])
+def test_ordering_paths(path):
+    """Occurrence counts across every ordering branch of the finish kernel (rank count
+    <= 256, bucket pass, skewed buckets -> block radix sort, > 8192 -> device sort),
+    with the occurrences spread over the text or packed into one stretch."""
+    rng = np.random.default_rng(57)
+    n = 1 << 20
+    for count, packed in [(2, False), (200, False), (300, False), (5000, False), (5000, True),
+                          (8192, False), (8192, True), (8193, True), (20000, False)]:
+        y = rng.integers(0, 4, n, dtype=np.uint8)           # bytes 0..3: "xy" never occurs
+        x = np.frombuffer(b"xy", np.uint8)
+        if packed:
+            start = int(rng.integers(0, n - 2 * count - 2))
+            ps = start + 2 * np.arange(count)
+        else:
+            ps = np.sort(rng.choice((n - 2) // 2, count, replace=False)) * 2
+        for p in ps:
+            y[p:p + 2] = x
+        want = oracle.brute(x, y)
+        assert len(want) == count
+        got = gpu(hc.prepare(x, 2, 12), to_dev(y, 3), path=path)
+        assert np.array_equal(got, want), (count, packed, len(got))
