@@ -40,7 +40,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-PATH_NAMES = {1: "staged", 2: "gather", 3: "stream"}
+PATH_NAMES = {1: "staged", 2: "gather", 3: "stream", 4: "shc"}
 sys.path.insert(0, ROOT)
 
 from paper_2310_15711_b200 import inputs as I  # noqa: E402

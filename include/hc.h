@@ -90,7 +90,9 @@ typedef enum hc_path {
     HC_PATH_AUTO = 0,   /* chosen from m, q */
     HC_PATH_STAGED = 1, /* text tiles staged in shared memory by TMA bulk copies */
     HC_PATH_GATHER = 2, /* no staging: lanes read only the q-grams they hash, from global memory */
-    HC_PATH_STREAM = 3  /* per-warp chunks staged in shared memory by 16-byte cp.async copies */
+    HC_PATH_STREAM = 3, /* per-warp chunks staged in shared memory by 16-byte cp.async copies */
+    HC_PATH_SHC = 4     /* Sentinel Hash Chain (Fig. 5 right): per-lane ranges copied into shared-
+                           memory boxes followed by a copy of x, SHC's fast loop per lane */
 } hc_path;
 
 typedef struct hc_search_opts {

@@ -174,12 +174,14 @@ constexpr uint32_t kDefaultSegPerLane = 2;
 constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per warp chunk
 constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
 constexpr uint32_t kDefaultStreamWarps = 8;     // stream path: warps per CTA
+constexpr uint32_t kShcLaneBytes = 128;         // SHC path: text bytes per lane and chunk
 
 cudaError_t launch_search(int path, const hc::KParams &p, cudaStream_t st, const hc_search_opts &o,
                           hc::LaunchInfo *li) {
     switch (path) {
     case HC_PATH_STAGED: return hc::launch_staged(p, st, o.max_ctas, o.ctas_per_sm, li);
     case HC_PATH_STREAM: return hc::launch_stream(p, st, o.max_ctas, o.ctas_per_sm, li);
+    case HC_PATH_SHC: return hc::launch_shc(p, st, o.max_ctas, o.ctas_per_sm, li);
     default: return hc::launch_gather(p, st, o.max_ctas, o.ctas_per_sm, li);
     }
 }
@@ -258,6 +260,29 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps) >
             max_smem_optin(h->device))
             path = HC_PATH_GATHER;
+    }
+    if (path == HC_PATH_SHC) {
+        // each lane owns c consecutive segments (about kShcLaneBytes of text)
+        const uint32_t lane_target = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) / 32
+                                                      : kShcLaneBytes;
+        const uint32_t c = std::max<uint32_t>(1u, (lane_target + S / 2) / S);
+        p.shc = 1;
+        p.seg_per_chunk = 32 * c;
+        p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
+        p.stages = 2;
+        // chunk bytes [a_k0 - m + 1, a_k1 - 1] plus alignment slack
+        p.stage_bytes = (p.seg_per_chunk * S + m + 48 + 15) & ~15u;
+        // box: the lane's bytes (c S + m - 1) in whole 16-byte words, then x (m) and the
+        // 8-byte word reads around its end
+        p.slot_bytes = (c * S + 2 * m + 40 + 15) & ~15u;
+        uint32_t nw = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps)
+                                                                : kDefaultStreamWarps;
+        while (nw > 1 && hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) >
+                             max_smem_optin(h->device))
+            --nw;
+        if (hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) > max_smem_optin(h->device))
+            return HC_EINVAL;   // m too long for per-lane boxes
+        p.block_warps = nw;
     }
     if (path == HC_PATH_GATHER) {
         const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)

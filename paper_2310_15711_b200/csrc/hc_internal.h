@@ -28,7 +28,8 @@ struct KParams {
     // gather path
     uint32_t seg_per_chunk; // segments per warp chunk
     uint32_t nchunks;
-    uint32_t block_warps;   // stream path: warps per CTA
+    uint32_t block_warps;   // stream / SHC paths: warps per CTA
+    uint32_t shc;           // SHC path (chunk geometry: whole segments)
     // output
     uint32_t *out;       // positions (window starts), unordered; NULL = count only
     uint32_t cap;        // capacity of out
@@ -48,6 +49,8 @@ cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int c
                           LaunchInfo *li);
 cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
+cudaError_t launch_shc(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                       LaunchInfo *li);
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
 // One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,
@@ -64,6 +67,8 @@ constexpr uint32_t kSmallSort = 8192;
 int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
                       uint32_t slot_bytes, uint32_t nbox);
 int gather_smem_bytes(uint32_t alpha, uint32_t m);
+int shc_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t box_bytes,
+                   uint32_t nwarps);
 int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs, uint32_t nwarps);
 
 constexpr int kStagedThreads = 256;

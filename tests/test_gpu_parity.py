@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
 from paper_2310_15711_b200 import hc  # noqa: E402
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
-PATHS = [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_AUTO]
+PATHS = [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC, hc.PATH_AUTO]
 
 
 def to_dev(y: np.ndarray, offset: int = 0):
@@ -80,7 +80,7 @@ def test_random_small(path):
         assert np.array_equal(got, want), (trial, m, q, alpha, n, off, len(want), len(got))
 
 
-@pytest.mark.parametrize("path", [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM])
+@pytest.mark.parametrize("path", [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC])
 @pytest.mark.parametrize("max_ctas,stages", [(1, 2), (2, 3), (3, 4), (5, 1)])
 def test_many_tiles_per_cta(path, max_ctas, stages):
     # tiny tiles / few CTAs: every CTA cycles its TMA ring many times
@@ -267,7 +267,7 @@ def test_search_batch_matches_single_searches():
     assert cnts == [len(w) for w in want]
 
 
-@pytest.mark.parametrize("path", [hc.PATH_STREAM, hc.PATH_GATHER])
+@pytest.mark.parametrize("path", [hc.PATH_STREAM, hc.PATH_GATHER, hc.PATH_SHC])
 def test_ordering_paths(path):
     """Occurrence counts across every ordering branch of the finish kernel (rank count
     <= 256, bucket pass, skewed buckets -> block radix sort, > 8192 -> device sort),

@@ -19,7 +19,7 @@ import torch  # noqa: E402
 from paper_2310_15711_b200 import hc  # noqa: E402
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
-NAMES = {1: "staged", 2: "gather", 3: "stream"}
+NAMES = {1: "staged", 2: "gather", 3: "stream", 4: "shc"}
 
 
 def main():
