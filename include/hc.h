@@ -114,6 +114,7 @@ typedef struct hc_search_opts {
     int trace_tiles;
     int surv_warps;   /* staged: survivor/producer warps per CTA (0 = default) */
     int block_warps;  /* stream: warps per CTA, 1..8 (0 = default 8) */
+    int no_multi;     /* hc_search_batch: 1 = no multi-pattern launches (each pattern alone) */
 } hc_search_opts;
 
 typedef struct hc_search_stats {

@@ -175,6 +175,9 @@ constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per w
 constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
 constexpr uint32_t kDefaultStreamWarps = 8;     // stream path: warps per CTA
 constexpr uint32_t kShcLaneBytes = 128;         // SHC path: text bytes per lane and chunk
+// hc_search_batch: patterns of equal (m, q, alpha) with shifts up to this share one
+// streamed pass over the text (multi-pattern stream kernel)
+constexpr uint32_t kMultiMaxShift = 32;
 
 cudaError_t launch_search(int path, const hc::KParams &p, cudaStream_t st, const hc_search_opts &o,
                           hc::LaunchInfo *li) {
@@ -308,16 +311,19 @@ struct BatchRes {
 };
 thread_local BatchRes g_batch[8];
 
+// Batch scratch of one pool stream: [kMaxPatterns counters of 16 B | positions], the
+// positions of a multi-pattern launch's pattern g at offset g * (cap / npat).
+constexpr size_t kCtrWords = 4 * hc::kMaxPatterns;
 cudaError_t batch_scratch(Scratch &sc, size_t cap) {
     if (!sc.buf || sc.cap < cap) {
         if (sc.buf) cudaFree(sc.buf);
         sc.buf = nullptr;
-        cudaError_t e = cudaMalloc(&sc.buf, 16 + cap * sizeof(uint32_t));
+        cudaError_t e = cudaMalloc(&sc.buf, (kCtrWords + cap) * sizeof(uint32_t));
         if (e != cudaSuccess) {
             sc.cap = 0;
             return e;
         }
-        e = cudaMemset(sc.buf, 0, 16);
+        e = cudaMemset(sc.buf, 0, kCtrWords * sizeof(uint32_t));
         if (e != cudaSuccess) return e;
         sc.cap = cap;
     }
@@ -605,40 +611,106 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
     cudaEventRecord(r->ev[kBatchStreams], stream);
     for (int j = 0; j < kBatchStreams; ++j) cudaStreamWaitEvent(r->st[j], r->ev[kBatchStreams], 0);
 
-    std::vector<uint8_t> redo(npat, 0);
     std::vector<size_t> caps(npat, 0);
     int launches = 0;
-    for (size_t i = 0; i < npat; ++i) {
+    int nlaunch = 0;   // search launches so far (round-robin over the pool streams)
+    auto same_shape = [&](const hc_handle *a, const hc_handle *b) {
+        return a->m == b->m && a->q == b->q && a->alpha == b->alpha;
+    };
+    for (size_t i = 0; i < npat;) {
         const hc_handle *h = hs[i];
         r->hcounts[i] = 0xffffffffu;
         if (n < h->m) {
             r->hcounts[i] = 0;
+            ++i;
             continue;
         }
         const size_t windows = n - h->m + 1;
-        const size_t mo = max_out ? max_out[i] : 0;
-        const bool want_pos = pos_out && pos_out[i] && mo > 0;
+        const uint32_t S = h->m - h->q + 1;
+        // multi-pattern launch: the next patterns of the same (m, q, alpha)
+        size_t g = 1;
+        const bool multi_ok = !o.no_multi && S <= kMultiMaxShift &&
+                              (o.path == HC_PATH_AUTO || o.path == HC_PATH_STREAM);
+        if (multi_ok)
+            while (i + g < npat && g < static_cast<size_t>(hc::kMaxPatterns) && hs[i + g] &&
+                   n >= hs[i + g]->m && same_shape(h, hs[i + g]))
+                ++g;
+        const int j = nlaunch++ % kBatchStreams;
+        Scratch &sc = r->sc[j];
         hc::KParams p{};
         int path = 0;
-        const int rc = setup_search(h, y_dev, nn, o, p, path);
-        if (rc != HC_OK) return fail(rc);
-        const int j = static_cast<int>(i % kBatchStreams);
-        Scratch &sc = r->sc[j];
-        const size_t cap = want_pos ? std::min<size_t>(std::max<size_t>(mo, size_t(1) << 16), windows) : 0;
-        e = batch_scratch(sc, std::max<size_t>(cap, 1));
+        if (g > 1) {
+            // stream geometry; all g F tables in one CTA's shared memory: 16 warps per CTA
+            // and 2 KiB chunks when more than two share it, else the stream defaults
+            hc_search_opts og = o;
+            og.path = HC_PATH_STREAM;
+            for (; g > 1; --g) {
+                og.tile_bytes = o.tile_bytes == 0 && g > 2 ? 2048 : o.tile_bytes;
+                const int rc = setup_search(h, y_dev, nn, og, p, path);
+                if (rc != HC_OK) return fail(rc);
+                if (path != HC_PATH_STREAM) continue;
+                p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
+                                                  : (g > 2 ? 16u : p.block_warps);
+                if (p.stages > 3) p.stages = 3;
+                if (hc::mstream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.block_warps,
+                                           static_cast<uint32_t>(g), p.stages) <=
+                    max_smem_optin(dev) - 2048)   // (the kernel's static shared memory)
+                    break;
+            }
+        }
+        if (g == 1) {
+            const int rc = setup_search(h, y_dev, nn, o, p, path);
+            if (rc != HC_OK) return fail(rc);
+        }
+        // per-pattern position capacity
+        size_t cap = 0;
+        for (size_t t = 0; t < g; ++t) {
+            const size_t mo = max_out ? max_out[i + t] : 0;
+            if (pos_out && pos_out[i + t] && mo > 0)
+                cap = std::max(cap, std::min<size_t>(std::max<size_t>(mo, size_t(1) << 16), windows));
+        }
+        e = batch_scratch(sc, std::max<size_t>(cap * g, 1));
         if (e != cudaSuccess) return cuda_fail(e, "batch scratch");
-        caps[i] = cap;
-        p.counter = sc.buf;
-        p.out = want_pos ? sc.buf + 4 : nullptr;
-        p.cap = static_cast<uint32_t>(cap);
         hc::LaunchInfo li;
-        e = launch_search(path, p, r->st[j], o, &li);
-        if (e == cudaSuccess)
-            e = hc::launch_finish(sc.buf, p.out, p.cap, want_pos ? pos_out[i] : nullptr,
+        if (g == 1) {
+            const size_t mo = max_out ? max_out[i] : 0;
+            const bool want_pos = pos_out && pos_out[i] && mo > 0;
+            caps[i] = want_pos ? cap : 0;
+            p.counter = sc.buf;
+            p.out = want_pos ? sc.buf + kCtrWords : nullptr;
+            p.cap = static_cast<uint32_t>(caps[i]);
+            e = launch_search(path, p, r->st[j], o, &li);
+        } else {
+            hc::MParams mp{};
+            mp.npat = static_cast<uint32_t>(g);
+            for (size_t t = 0; t < g; ++t) {
+                const hc_handle *ht = hs[i + t];
+                const size_t mo = max_out ? max_out[i + t] : 0;
+                const bool want_pos = pos_out && pos_out[i + t] && mo > 0;
+                caps[i + t] = want_pos ? cap : 0;
+                mp.F[t] = ht->dF;
+                mp.x[t] = ht->dx;
+                mp.hv[t] = ht->hv;
+                mp.counter[t] = sc.buf + 4 * t;
+                mp.out[t] = want_pos ? sc.buf + kCtrWords + t * cap : nullptr;
+                mp.cap[t] = static_cast<uint32_t>(caps[i + t]);
+            }
+            e = hc::launch_mstream(p, mp, r->st[j], o.max_ctas, o.ctas_per_sm, &li);
+        }
+        ++launches;
+        for (size_t t = 0; t < g && e == cudaSuccess; ++t) {
+            const size_t mo = max_out ? max_out[i + t] : 0;
+            const bool want_pos = pos_out && pos_out[i + t] && mo > 0;
+            uint32_t *ctr = sc.buf + 4 * t;
+            const uint32_t *pos = want_pos ? sc.buf + kCtrWords + t * cap : nullptr;
+            e = hc::launch_finish(ctr, pos, static_cast<uint32_t>(caps[i + t]),
+                                  want_pos ? pos_out[i + t] : nullptr,
                                   want_pos ? static_cast<uint32_t>(std::min<size_t>(mo, windows)) : 0u,
-                                  p.n, r->hcounts_dev + i, r->st[j]);
+                                  p.n, r->hcounts_dev + i + t, r->st[j]);
+            ++launches;
+        }
         if (e != cudaSuccess) return cuda_fail(e, "batch launch");
-        launches += 2;
+        i += g;
     }
     for (int j = 0; j < kBatchStreams; ++j) {
         cudaEventRecord(r->ev[j], r->st[j]);

@@ -40,6 +40,19 @@ struct KParams {
     uint32_t trace_tiles;       // tiles per CTA recorded
 };
 
+// Per-pattern parameters of a multi-pattern launch (stream path, patterns sharing
+// m, q, alpha): the text is staged once and filtered for every pattern.
+constexpr int kMaxPatterns = 4;
+struct MParams {
+    uint32_t npat;
+    const uint32_t *F[kMaxPatterns];
+    const uint8_t *x[kMaxPatterns];
+    uint32_t hv[kMaxPatterns];
+    uint32_t *counter[kMaxPatterns];
+    uint32_t *out[kMaxPatterns];
+    uint32_t cap[kMaxPatterns];
+};
+
 struct LaunchInfo {
     int grid = 0, block = 0, smem = 0;
 };
@@ -51,6 +64,10 @@ cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int c
                           LaunchInfo *li);
 cudaError_t launch_shc(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                        LaunchInfo *li);
+cudaError_t launch_mstream(const KParams &p, const MParams &mp, cudaStream_t st, int max_ctas,
+                           int ctas_per_sm, LaunchInfo *li);
+int mstream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t nwarps, uint32_t npat,
+                       uint32_t bufs);
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
 // One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,

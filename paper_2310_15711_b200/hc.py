@@ -42,7 +42,7 @@ class Opts(C.Structure):
                 ("seg_per_lane", C.c_int), ("max_ctas", C.c_int), ("time_kernel", C.c_int),
                 ("ctas_per_sm", C.c_int), ("debug", C.c_int), ("tma_chunk", C.c_int),
                 ("trace", C.c_void_p), ("trace_tiles", C.c_int), ("surv_warps", C.c_int),
-                ("block_warps", C.c_int)]
+                ("block_warps", C.c_int), ("no_multi", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -183,9 +183,9 @@ def prepare(x, q: int, alpha: int) -> Handle:
 
 def _opts(path=PATH_AUTO, tile_bytes=0, stages=0, seg_per_lane=0, max_ctas=0, time_kernel=0,
           ctas_per_sm=0, debug=0, tma_chunk=0, trace=0, trace_tiles=0, surv_warps=0,
-          block_warps=0):
+          block_warps=0, no_multi=0):
     return Opts(path, tile_bytes, stages, seg_per_lane, max_ctas, int(time_kernel), ctas_per_sm,
-                debug, tma_chunk, trace or None, trace_tiles, surv_warps, block_warps)
+                debug, tma_chunk, trace or None, trace_tiles, surv_warps, block_warps, int(no_multi))
 
 
 def search_raw(h: Handle, y_ptr: int, n: int, pos_ptr: int | None, max_out: int,

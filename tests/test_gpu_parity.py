@@ -289,3 +289,39 @@ def test_ordering_paths(path):
         assert len(want) == count
         got = gpu(hc.prepare(x, 2, 12), to_dev(y, 3), path=path)
         assert np.array_equal(got, want), (count, packed, len(got))
+
+
+@pytest.mark.parametrize("no_multi", [0, 1])
+def test_search_batch_multi_pattern_groups(no_multi):
+    """Multi-pattern launches (patterns sharing m, q, alpha filtered in one pass over the
+    text): groups of 1..4 and a partial last group, patterns with many occurrences (one
+    over the scratch, one over the in-kernel ordering bound), absent patterns,
+    overlapping occurrences, unaligned text; every result equals brute force."""
+    rng = np.random.default_rng(73)
+    y = I.gen_text("dna", 3_000_017, 73)
+    yy = y.copy()
+    pats = []
+    for m, q, a, count in [(8, 4, 12, 9), (16, 6, 12, 6), (16, 3, 11, 5), (32, 6, 12, 3), (4, 2, 10, 2),
+                           (24, 8, 12, 5)]:
+        for t in range(count):
+            o = int(rng.integers(0, len(y) - m))
+            x = y[o:o + m].copy()
+            if t == 1:
+                x = rng.permutation(x)                           # likely absent
+            for p in rng.integers(0, len(y) - m, int(rng.integers(0, 9))):
+                yy[p:p + m] = x
+            pats.append((x, q, a))
+    # very frequent patterns inside a group (count > 8192 and > the 65536 scratch)
+    pats.insert(3, (np.frombuffer(b"AAAA", np.uint8), 2, 12))
+    yy[1000:1000 + 300_000] = ord("A")
+    pats.insert(5, (np.frombuffer(b"ACGT", np.uint8), 2, 12))
+    yd = to_dev(yy, 5)
+    hs = [hc.prepare(x, q, a) for x, q, a in pats]
+    want = [oracle.brute(x, yy) for x, _, _ in pats]
+    got = hc.search_batch(hs, yd, no_multi=no_multi)
+    torch.cuda.synchronize()
+    for k, (g, w) in enumerate(zip(got, want)):
+        assert np.array_equal(g.cpu().numpy(), w), (k, len(g), len(w))
+    got = hc.search_batch(hs, yd, max_out=3, no_multi=no_multi)
+    for g, w in zip(got, want):
+        assert np.array_equal(g.cpu().numpy(), w[:3])

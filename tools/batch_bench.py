@@ -44,16 +44,21 @@ def main():
             hc.search_raw(h, y.data_ptr(), n, pos.data_ptr(), cap, sp, o, st)
             single += st.kernel_ms
         outs = [torch.empty(cap, dtype=torch.int64, device="cuda") for _ in hs]
-        best = None
-        for _ in range(3):
-            flush.view(torch.int64).sum()
-            got = hc.search_batch_raw(hs, y.data_ptr(), n, [t.data_ptr() for t in outs],
-                                      [cap] * len(hs), sp, o, st)
-            assert got == cnt
-            best = st.kernel_ms if best is None else min(best, st.kernel_ms)
-        ps, pb = single / len(hs) * 1e3, best / len(hs) * 1e3
-        print(f"m={m}: single {ps:.1f} us/pattern ({n / ps / 1e3:.0f} GB/s), batch "
-              f"{pb:.1f} us/pattern ({n / pb / 1e3:.0f} GB/s)", flush=True)
+        res = {}
+        for nm in (0, 1):
+            ob = hc.Opts(path=0, time_kernel=1, no_multi=nm)
+            best = None
+            for _ in range(3):
+                flush.view(torch.int64).sum()
+                got = hc.search_batch_raw(hs, y.data_ptr(), n, [t.data_ptr() for t in outs],
+                                          [cap] * len(hs), sp, ob, st)
+                assert got == cnt
+                best = st.kernel_ms if best is None else min(best, st.kernel_ms)
+            res[nm] = best / len(hs) * 1e3
+        ps = single / len(hs) * 1e3
+        print(f"m={m}: single {ps:.1f} us/pattern ({n / ps / 1e3:.0f} GB/s), batch multi "
+              f"{res[0]:.1f} us/pattern ({n / res[0] / 1e3:.0f} GB/s), batch no-multi "
+              f"{res[1]:.1f} us/pattern ({n / res[1] / 1e3:.0f} GB/s)", flush=True)
 
 
 if __name__ == "__main__":
