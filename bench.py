@@ -495,7 +495,8 @@ def main():
             if use_batch and args.api == "batch":
                 for m, idx in by_m.items():
                     t_m = time.perf_counter()
-                    hs = [hc.prepare(work[k][4], work[k][1], work[k][2]) for k in idx]
+                    hs = hc.prepare_batch([work[k][4] for k in idx], work[idx[0]][1],
+                                          work[idx[0]][2])
                     got = hc.search_batch_raw(hs, ydev.data_ptr(), n,
                                               [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp)
                     for k, c in zip(idx, got):
@@ -538,7 +539,7 @@ def main():
         e2e_bytes = n * len(work) * e2e_steps * (1 if shard_mode else ws)
         line["e2e"] = {"value": round(e2e_bytes / t_e2e / 1e9, 1), "unit": "GB/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "includes": "pinned H2D of the text, hc_prepare of every pattern, "
+                       "includes": "pinned H2D of the text, hc_prepare(_batch) of every pattern, "
                                    + ("hc_search_batch per m" if (use_batch and args.api == "batch")
                                       else "hc_search per pattern")
                                    + ", D2H of counts and positions; wall clock"}

@@ -66,6 +66,16 @@ typedef struct hc_handle hc_handle;
  * Returns a new handle (free with hc_destroy) or NULL (see hc_last_error()). */
 hc_handle *hc_prepare(const uint8_t *x, size_t m, int q, int alpha);
 
+/* Preprocessing of P patterns at once (the paper times Preprocessing with every search,
+ * P:380; a batch of searches amortises its uploads): Fig. 3 for each xs[i] (length
+ * ms[i], HOST memory, copied) with the same q and alpha, then ONE device allocation and
+ * ONE host-to-device copy for all the tables and patterns.  hs_out[i] receives the
+ * handle of xs[i]; each is used and destroyed like an hc_prepare handle (the shared
+ * device block is freed with the last of them).  Returns HC_OK, or a negative
+ * hc_status (parameter checks as hc_prepare, per pattern) with no handle created. */
+int hc_prepare_batch(const uint8_t *const *xs, const size_t *ms, size_t P, int q, int alpha,
+                     hc_handle **hs_out);
+
 /* Code of the last failure on this host thread (HC_OK if none). */
 int hc_last_error(void);
 

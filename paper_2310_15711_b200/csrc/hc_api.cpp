@@ -19,6 +19,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <memory>
 #include <vector>
 
 #include "hc.h"
@@ -31,6 +32,7 @@ struct hc_handle {
     int device = 0;
     uint32_t *dF = nullptr;
     uint8_t *dx = nullptr;
+    std::shared_ptr<void> block;   // hc_prepare_batch: device block shared by the batch
 };
 
 namespace {
@@ -437,10 +439,104 @@ hc_handle *hc_prepare(const uint8_t *x, size_t m, int q, int alpha) {
     return h;
 }
 
+// Device blocks of hc_prepare_batch are recycled (size classes of powers of two, per
+// device) instead of cudaMalloc / cudaFree per batch: cudaFree synchronises the device
+// and both calls showed multi-millisecond outliers in the end-to-end loop.
+namespace {
+std::mutex g_block_mu;
+std::vector<std::pair<size_t, void *>> g_block_pool[8];
+void *block_get(int dev, size_t bytes, size_t *cls) {
+    size_t c = 4096;
+    while (c < bytes) c <<= 1;
+    *cls = c;
+    {
+        std::lock_guard<std::mutex> lk(g_block_mu);
+        auto &pool = g_block_pool[dev & 7];
+        for (size_t i = 0; i < pool.size(); ++i)
+            if (pool[i].first == c) {
+                void *p = pool[i].second;
+                pool.erase(pool.begin() + static_cast<long>(i));
+                return p;
+            }
+    }
+    void *p = nullptr;
+    return cudaMalloc(&p, c) == cudaSuccess ? p : nullptr;
+}
+void block_put(int dev, size_t cls, void *p) {
+    std::lock_guard<std::mutex> lk(g_block_mu);
+    auto &pool = g_block_pool[dev & 7];
+    if (pool.size() < 64) pool.emplace_back(cls, p);
+    else cudaFree(p);
+}
+}  // namespace
+
+int hc_prepare_batch(const uint8_t *const *xs, const size_t *ms, size_t P, int q, int alpha,
+                     hc_handle **hs_out) {
+    if (P == 0) return HC_OK;
+    if (!xs || !ms || !hs_out) return fail(HC_EINVAL);
+    for (size_t i = 0; i < P; ++i) {
+        const int rc = check_params(xs[i], ms[i], q, alpha);
+        if (rc != HC_OK) return fail(rc);
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaGetDevice");
+        return fail(HC_ENODEV);
+    }
+    // host tables (Fig. 3 per pattern), laid out as the device block: F | x per pattern
+    const size_t fbytes = (size_t(1) << alpha) * sizeof(uint32_t);
+    std::vector<size_t> off(P + 1, 0);
+    for (size_t i = 0; i < P; ++i) off[i + 1] = off[i] + ((fbytes + 15) & ~size_t(15)) + ((ms[i] + 16 + 15) & ~size_t(15));
+    std::vector<hc_handle *> hs(P, nullptr);
+    std::vector<uint8_t> staging(off[P], 0);
+    for (size_t i = 0; i < P; ++i) {
+        hc_handle *h = new (std::nothrow) hc_handle();
+        if (!h) {
+            for (hc_handle *t : hs) delete t;
+            return fail(HC_ENOMEM);
+        }
+        hs[i] = h;
+        h->m = static_cast<uint32_t>(ms[i]);
+        h->q = static_cast<uint32_t>(q);
+        h->alpha = static_cast<uint32_t>(alpha);
+        h->mask = (1u << alpha) - 1u;
+        h->device = dev;
+        h->x.assign(xs[i], xs[i] + ms[i]);
+        h->F.assign(size_t(1) << alpha, 0u);
+        build_table(xs[i], h->m, h->q, h->alpha, h->F.data(), &h->s, &h->hv);
+        std::memcpy(staging.data() + off[i], h->F.data(), fbytes);
+        std::memcpy(staging.data() + off[i] + ((fbytes + 15) & ~size_t(15)), xs[i], ms[i]);
+    }
+    size_t cls = 0;
+    void *blk = block_get(dev, off[P], &cls);
+    e = blk ? cudaMemcpy(blk, staging.data(), off[P], cudaMemcpyHostToDevice) : cudaErrorMemoryAllocation;
+    if (e != cudaSuccess) {
+        if (blk) block_put(dev, cls, blk);
+        for (hc_handle *t : hs) delete t;
+        return cuda_fail(e, "hc_prepare_batch upload");
+    }
+    // the block goes back to the pool with the last handle (searches using it are
+    // complete by then: the caller must not destroy a handle while a search on it is
+    // in flight, as for hc_prepare handles)
+    std::shared_ptr<void> block(blk, [dev, cls](void *p) { block_put(dev, cls, p); });
+    for (size_t i = 0; i < P; ++i) {
+        uint8_t *base = static_cast<uint8_t *>(blk) + off[i];
+        hs[i]->dF = reinterpret_cast<uint32_t *>(base);
+        hs[i]->dx = base + ((fbytes + 15) & ~size_t(15));
+        hs[i]->block = block;
+        hs_out[i] = hs[i];
+    }
+    g_last_error = HC_OK;
+    return HC_OK;
+}
+
 void hc_destroy(hc_handle *h) {
     if (!h) return;
-    if (h->dF) cudaFree(h->dF);
-    if (h->dx) cudaFree(h->dx);
+    if (!h->block) {   // hc_prepare: own allocations (batch handles share h->block)
+        if (h->dF) cudaFree(h->dF);
+        if (h->dx) cudaFree(h->dx);
+    }
     delete h;
 }
 

@@ -33,7 +33,7 @@ WORD_BITS = 32
 
 # the symbols include/hc.h declares (tests check every one is exported)
 EXPORTS = ("hc_prepare", "hc_last_error", "hc_strerror", "hc_search", "hc_search_ex",
-           "hc_search_batch", "hc_search_host", "hc_destroy", "hc_table", "hc_build_table",
+           "hc_search_batch", "hc_prepare_batch", "hc_search_host", "hc_destroy", "hc_table", "hc_build_table",
            "hc_version")
 
 
@@ -73,6 +73,9 @@ _lib.hc_search_batch.argtypes = [C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, 
                                  C.POINTER(C.c_size_t), C.c_void_p, C.POINTER(Opts),
                                  C.POINTER(Stats)]
 _lib.hc_search_batch.restype = C.c_int
+_lib.hc_prepare_batch.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_size_t, C.c_int,
+                                  C.c_int, C.POINTER(C.c_void_p)]
+_lib.hc_prepare_batch.restype = C.c_int
 _lib.hc_search_host.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                                 C.c_void_p]
 _lib.hc_search_host.restype = C.c_int64
@@ -179,6 +182,28 @@ class Handle:
 
 def prepare(x, q: int, alpha: int) -> Handle:
     return Handle(x, q, alpha)
+
+
+def prepare_batch(xs, q: int, alpha: int) -> list:
+    """hc_prepare_batch: Preprocessing of every pattern in xs (same q, alpha) with one
+    device allocation and one upload; returns one Handle per pattern."""
+    arrs = [_bytes(x) for x in xs]
+    P = len(arrs)
+    if P == 0:
+        return []
+    ptrs = (C.c_void_p * P)(*[a.ctypes.data if len(a) else None for a in arrs])
+    ms = (C.c_size_t * P)(*[len(a) for a in arrs])
+    out = (C.c_void_p * P)()
+    rc = _lib.hc_prepare_batch(ptrs, ms, P, q, alpha, out)
+    if rc != HC_OK:
+        raise HCError(int(rc), "hc_prepare_batch")
+    hs = []
+    for a, ptr in zip(arrs, out):
+        h = Handle.__new__(Handle)
+        h.m, h.q, h.alpha, h.x = len(a), q, alpha, a.tobytes()
+        h._h = C.c_void_p(ptr)
+        hs.append(h)
+    return hs
 
 
 def _opts(path=PATH_AUTO, tile_bytes=0, stages=0, seg_per_lane=0, max_ctas=0, time_kernel=0,

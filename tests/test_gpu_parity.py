@@ -325,3 +325,32 @@ def test_search_batch_multi_pattern_groups(no_multi):
     got = hc.search_batch(hs, yd, max_out=3, no_multi=no_multi)
     for g, w in zip(got, want):
         assert np.array_equal(g.cpu().numpy(), w[:3])
+
+
+def test_prepare_batch_equals_prepare():
+    """hc_prepare_batch: same tables and H_v as hc_prepare for every pattern, the same
+    search results, and handles usable and destroyable in any order."""
+    rng = np.random.default_rng(75)
+    y = I.gen_text("protein", 500_009, 75)
+    for q, a in [(3, 11), (6, 12), (1, 8), (8, 15)]:
+        xs = []
+        for _ in range(7):
+            m = int(rng.integers(q, 90))
+            o = int(rng.integers(0, len(y) - m))
+            xs.append(y[o:o + m].copy())
+        hb = hc.prepare_batch(xs, q, a)
+        yd = to_dev(y, 1)
+        for x, h in zip(xs, hb):
+            t1, t2 = h.table(), hc.prepare(x, q, a).table()
+            assert np.array_equal(t1.F, t2.F) and t1.hv == t2.hv and t1.s == t2.s
+            assert np.array_equal(gpu(h, yd), oracle.brute(x, y))
+        got = hc.search_batch(hb, yd)
+        for x, g in zip(xs, got):
+            assert np.array_equal(g.cpu().numpy(), oracle.brute(x, y))
+        for h in hb[::2]:
+            h.close()
+        assert np.array_equal(gpu(hb[1], yd), oracle.brute(xs[1], y))
+        for h in hb[1::2]:
+            h.close()
+    with pytest.raises(hc.HCError):
+        hc.prepare_batch([b"abc", b"a"], 2, 8)       # q > m for the second pattern
