@@ -1108,12 +1108,15 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
                                           reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
                                           0u, 0u, wo, lane};
     const uint32_t total_warps = gridDim.x * NW;
+    if (warp == 0 && lane == 0) trace_event(p, 0, 0);          // table loaded
     for (uint32_t c = blockIdx.x * NW + warp; c < p.nchunks; c += total_warps) {
         const uint32_t seg_lo = c * p.seg_per_chunk;
         const uint32_t seg_hi = min(seg_lo + p.seg_per_chunk, p.K);
         filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
     }
+    if (warp == 0 && lane == 0) trace_event(p, 0, 1);          // lattice filtered
     sink.drain();
+    if (warp == 0 && lane == 0) trace_event(p, 0, 2);          // survivors done
     wo.flush(p, lane);
     if (lane == 0) trace_cta(p, 1);   // last warp to get here wins
 }

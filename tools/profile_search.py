@@ -94,7 +94,18 @@ def main():
                   f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}"
                   + (f" phaseB iters={st['dbg'][0]} calls={st['dbg'][1]}" if args.debug == 5 else ""),
                   flush=True)
-            if args.trace and r == args.reps - 1:
+            if args.trace and r == args.reps - 1 and st["path"] == 2:
+                import numpy as np
+                g = st["grid"]
+                a = tr[:g * args.trace * 4].view(g, args.trace, 4)[:, 0, :3].cpu().numpy().astype(np.float64)
+                ce = tr[g * args.trace * 4: g * args.trace * 4 + 2 * g].view(g, 2).cpu().numpy().astype(np.float64)
+                t0 = ce[:, 0].min()
+                rel = lambda v: (v - t0) / 1e3
+                for nm, v in [("entry", ce[:, 0]), ("table loaded", a[:, 0]), ("filtered", a[:, 1]),
+                              ("survivors done", a[:, 2]), ("exit", ce[:, 1])]:
+                    r_ = rel(v)
+                    print(f"  gather warp0 {nm}: p50 {np.median(r_):.2f} p90 {np.percentile(r_, 90):.2f} max {r_.max():.2f} us")
+            elif args.trace and r == args.reps - 1:
                 analyze_trace(tr, st["grid"], args.trace, args.stages or 3)
                 if args.debug == 11:
                     import numpy as np
