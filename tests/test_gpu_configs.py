@@ -74,3 +74,18 @@ def test_c5_stress_closed_form():
             want = oracle.brute_threaded(x, y[lo:hi]) + lo
             sel = got[(got >= lo) & (got <= hi - m)]
             assert np.array_equal(sel, want)
+
+
+def test_c2_batch_multi_pattern_full():
+    """The bench's batch launch configuration at full size: hc_search_batch over C2's
+    text with 4 patterns per m (one multi-pattern launch each for m <= 32), every
+    result equal to the brute-force oracle."""
+    cfg = I.CONFIGS["C2"]
+    y, block = I.config_text(cfg)
+    yd = torch.from_numpy(y).cuda()
+    for m in (8, 16, 32, 64):
+        q, a = cfg.qa[m]
+        pats = [x for _, x in I.patterns(cfg, y, m, block=block)[:4]]
+        got = hc.search_batch(hc.prepare_batch(pats, q, a), yd)
+        for x, g in zip(pats, got):
+            assert np.array_equal(g.cpu().numpy(), oracle.brute_threaded(x, y)), m

@@ -1,7 +1,7 @@
 #!/bin/bash
 # bench + ncu evidence for profiles/ (run on the GPU box)
 set -x
-timeout 300 python -m pytest tests/test_gpu_parity.py -q 2>&1 | tail -1 > gpurun_out/parity.txt
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -1 > gpurun_out/parity.txt
 timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 # launch list of one bench step (reduced: 5 patterns per m) -- cold-cache, serialised
 python bench.py --steps 1 --warmup 3 --per-m 5 --no-e2e --no-cpu > gpurun_out/bench_small.json 2> gpurun_out/bench_small.err && \
