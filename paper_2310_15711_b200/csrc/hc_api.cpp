@@ -180,6 +180,11 @@ constexpr uint32_t kShcLaneBytes = 128;         // SHC path: text bytes per lane
 // hc_search_batch: patterns of equal (m, q, alpha) with shifts up to this share one
 // streamed pass over the text (multi-pattern stream kernel)
 constexpr uint32_t kMultiMaxShift = 32;
+// ... and with the gather access (the patterns share the lattice's DRAM sectors) up to
+#ifndef HC_MULTI_GATHER_MAX_SHIFT
+#define HC_MULTI_GATHER_MAX_SHIFT 256
+#endif
+constexpr uint32_t kMultiGatherMaxShift = HC_MULTI_GATHER_MAX_SHIFT;
 
 cudaError_t launch_search(int path, const hc::KParams &p, cudaStream_t st, const hc_search_opts &o,
                           hc::LaunchInfo *li) {
@@ -725,8 +730,10 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
         const uint32_t S = h->m - h->q + 1;
         // multi-pattern launch: the next patterns of the same (m, q, alpha)
         size_t g = 1;
-        const bool multi_ok = !o.no_multi && S <= kMultiMaxShift &&
-                              (o.path == HC_PATH_AUTO || o.path == HC_PATH_STREAM);
+        const bool stream_multi = S <= kMultiMaxShift;
+        const int multi_path = stream_multi ? HC_PATH_STREAM : HC_PATH_GATHER;
+        const bool multi_ok = !o.no_multi && S <= kMultiGatherMaxShift &&
+                              (o.path == HC_PATH_AUTO || o.path == multi_path);
         if (multi_ok)
             while (i + g < npat && g < static_cast<size_t>(hc::kMaxPatterns) && hs[i + g] &&
                    n >= hs[i + g]->m && same_shape(h, hs[i + g]))
@@ -739,15 +746,23 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
             // stream geometry; all g F tables in one CTA's shared memory: 16 warps per CTA
             // and 2 KiB chunks when more than two share it, else the stream defaults
             hc_search_opts og = o;
-            og.path = HC_PATH_STREAM;
+            og.path = multi_path;
             for (; g > 1; --g) {
-                og.tile_bytes = o.tile_bytes == 0 && g > 2 ? 2048 : o.tile_bytes;
+                og.tile_bytes = stream_multi && o.tile_bytes == 0 && g > 2 ? 2048 : o.tile_bytes;
                 const int rc = setup_search(h, y_dev, nn, og, p, path);
                 if (rc != HC_OK) return fail(rc);
-                if (path != HC_PATH_STREAM) continue;
-                p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
-                                                  : (g > 2 ? 16u : p.block_warps);
-                if (p.stages > 3) p.stages = 3;
+                if (path != multi_path) continue;
+                if (stream_multi) {
+                    p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
+                                                      : (g > 2 ? 16u : p.block_warps);
+                    if (p.stages > 3) p.stages = 3;
+                } else {   // gather access, no stage buffers
+                    p.mgather = 1;
+                    p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
+                                                      : 8u;
+                    p.stage_bytes = 0;
+                    p.stages = 2;
+                }
                 if (hc::mstream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.block_warps,
                                            static_cast<uint32_t>(g), p.stages) <=
                     max_smem_optin(dev) - 2048)   // (the kernel's static shared memory)

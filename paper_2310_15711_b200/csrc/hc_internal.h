@@ -30,6 +30,7 @@ struct KParams {
     uint32_t nchunks;
     uint32_t block_warps;   // stream / SHC paths: warps per CTA
     uint32_t shc;           // SHC path (chunk geometry: whole segments)
+    uint32_t mgather;       // multi-pattern kernel without staging (gather access)
     // output
     uint32_t *out;       // positions (window starts), unordered; NULL = count only
     uint32_t cap;        // capacity of out

@@ -1426,7 +1426,8 @@ struct MWarp {   // one warp's per-pattern queues and output state (shared memor
     // global text (the queue spans chunks: survivors are drained 32 at a time, so each
     // pattern costs one L2 round trip per 32 survivors, not one per chunk); continuing
     // segments to pattern i's q2 (phase B on global text)
-    __device__ __forceinline__ void steps(uint32_t i, const SmemText &txt, uint32_t from,
+    template <class T>
+    __device__ __forceinline__ void steps(uint32_t i, const T &, uint32_t from,
                                           uint32_t cnt, const uint8_t *sx, uint32_t lane) const {
         __syncwarp();
         const bool act = lane < cnt;
@@ -1448,8 +1449,8 @@ struct MWarp {   // one warp's per-pattern queues and output state (shared memor
     }
 };
 
-template <int Q, int SH>
-__device__ __forceinline__ void mstream_filter(const KParams &p, const SmemText &txt, uint32_t P,
+template <int Q, int SH, class T>
+__device__ __forceinline__ void mstream_filter(const KParams &p, const T &txt, uint32_t P,
                                                uint32_t k0, uint32_t k1, uint32_t lane,
                                                const MWarp<Q, SH> &mw, const uint8_t *sx0,
                                                uint32_t xs) {
@@ -1525,7 +1526,7 @@ __device__ __forceinline__ void mstream_loop(const KParams &p, uint32_t P, const
         const StreamChunk g = stream_chunk(p, c);
         const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
         const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
-        mstream_filter<Q, SH>(p, txt, P, g.k0, g.k1, lane, mw, sx0, xs);
+        mstream_filter<Q, SH, SmemText>(p, txt, P, g.k0, g.k1, lane, mw, sx0, xs);
         __syncwarp();
         b = b + 1 == NB ? 0 : b + 1;
     }
@@ -1597,7 +1598,17 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
     const uint32_t total_warps = gridDim.x * NW;
     const uint32_t gw = blockIdx.x * NW + warp;
     const uint32_t bufs0 = smem_u32(smem + L.ring_off) + warp * p.stages * p.stage_bytes;
-    if (p.stages == 3)
+    if (p.mgather) {
+        // large shifts: no staging, the lattice q-grams are read from global memory (the
+        // gather path's access), hashed once and tested against every pattern: the
+        // patterns share the DRAM sectors the lattice touches
+        const GlobalText gtxt{p.y};
+        for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
+            const uint32_t k0 = c * p.seg_per_chunk;
+            mstream_filter<Q, SH, GlobalText>(p, gtxt, P, k0, min(k0 + p.seg_per_chunk, p.K), lane, mw,
+                                              sx0, L.x_stride);
+        }
+    } else if (p.stages == 3)
         mstream_loop<Q, SH, 3>(p, P, mw, sx0, L.x_stride, bufs0, gw, total_warps, lane);
     else
         mstream_loop<Q, SH, 2>(p, P, mw, sx0, L.x_stride, bufs0, gw, total_warps, lane);

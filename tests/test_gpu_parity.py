@@ -294,7 +294,8 @@ def test_ordering_paths(path):
 @pytest.mark.parametrize("no_multi", [0, 1])
 def test_search_batch_multi_pattern_groups(no_multi):
     """Multi-pattern launches (patterns sharing m, q, alpha filtered in one pass over the
-    text): groups of 1..4 and a partial last group, patterns with many occurrences (one
+    text; staged for shifts <= 32, gather access up to 256, single beyond): groups of
+    1..4 and a partial last group, patterns with many occurrences (one
     over the scratch, one over the in-kernel ordering bound), absent patterns,
     overlapping occurrences, unaligned text; every result equals brute force."""
     rng = np.random.default_rng(73)
@@ -302,7 +303,8 @@ def test_search_batch_multi_pattern_groups(no_multi):
     yy = y.copy()
     pats = []
     for m, q, a, count in [(8, 4, 12, 9), (16, 6, 12, 6), (16, 3, 11, 5), (32, 6, 12, 3), (4, 2, 10, 2),
-                           (24, 8, 12, 5)]:
+                           (24, 8, 12, 5), (64, 6, 12, 6), (100, 3, 11, 4), (250, 8, 12, 5),
+                           (300, 6, 12, 2)]:
         for t in range(count):
             o = int(rng.integers(0, len(y) - m))
             x = y[o:o + m].copy()

@@ -1,1 +1,2 @@
-for r in 1 2; do for v in base new; do echo "== $v"; HC_LIB=build_obj/libhc_$v.so python tools/batch_bench.py --patterns 20 --ms 8 16 32 64 256 2>&1; done; done > gpurun_out/exp.txt
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 > gpurun_out/parity.txt
+timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
