@@ -160,6 +160,9 @@ int max_smem_optin(int dev) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     return v > 0 ? v : 48 * 1024;
 }
+// dynamic shared memory a kernel may request: the opt-in maximum less the kernels'
+// static shared memory (s_params and the finish / sort buffers stay below 2 KiB)
+int smem_budget(int dev) { return max_smem_optin(dev) - 2048; }
 
 // Default path choice: stream the whole text through per-warp shared
 // buffers when the shift is small (the lattice is dense, every sector is read);
@@ -248,7 +251,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
             p.nbox = std::min<uint32_t>(64u, room / (2 * (p.slot_bytes + 8)));
         }
         const int smem = hc::staged_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
-        if (smem > max_smem_optin(h->device)) {
+        if (smem > smem_budget(h->device)) {
             if (o.path == HC_PATH_STAGED) return HC_EINVAL;
             path = HC_PATH_GATHER;
         }
@@ -268,13 +271,15 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         // shifts too long for per-warp buffers (S > ~200) take the gather path, which
         // reads only the q-grams it hashes anyway
         if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps) >
-            max_smem_optin(h->device))
+            smem_budget(h->device))
             path = HC_PATH_GATHER;
     }
     if (path == HC_PATH_SHC) {
         // each lane owns c consecutive segments (about kShcLaneBytes of text)
+        // (measured on C2: 32 bytes per lane for shifts <= 16, 256 above: 1.2-1.6x faster
+        // than a uniform 128)
         const uint32_t lane_target = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) / 32
-                                                      : kShcLaneBytes;
+                                                      : (S <= 16 ? 32u : 2 * kShcLaneBytes);
         const uint32_t c = std::max<uint32_t>(1u, (lane_target + S / 2) / S);
         p.shc = 1;
         p.seg_per_chunk = 32 * c;
@@ -288,9 +293,9 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         uint32_t nw = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps)
                                                                 : kDefaultStreamWarps;
         while (nw > 1 && hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) >
-                             max_smem_optin(h->device))
+                             smem_budget(h->device))
             --nw;
-        if (hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) > max_smem_optin(h->device))
+        if (hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) > smem_budget(h->device))
             return HC_EINVAL;   // m too long for per-lane boxes
         p.block_warps = nw;
     }
@@ -299,7 +304,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
                                                 : (S >= 512 ? 1u : kDefaultSegPerLane);
         p.seg_per_chunk = 32 * spl;
         p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
-        if (hc::gather_smem_bytes(p.alpha, m) > max_smem_optin(h->device)) return HC_EINVAL;
+        if (hc::gather_smem_bytes(p.alpha, m) > smem_budget(h->device)) return HC_EINVAL;
     }
 
     return HC_OK;
@@ -765,7 +770,7 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
                 }
                 if (hc::mstream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.block_warps,
                                            static_cast<uint32_t>(g), p.stages) <=
-                    max_smem_optin(dev) - 2048)   // (the kernel's static shared memory)
+                    smem_budget(dev))
                     break;
             }
         }

@@ -1,2 +1,2 @@
-HC_LIB=build_obj/libhc_p8.so timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "batch" 2>&1 | tail -2 > gpurun_out/parity.txt
-for r in 1; do for v in p4 p8; do echo "== $v"; HC_LIB=build_obj/libhc_$v.so python tools/batch_bench.py --patterns 24 --ms 8 16 32 64 128 256 2>&1; done; done > gpurun_out/exp.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2 > gpurun_out/parity.txt
+for t in 0 8192; do echo "== shc tile=$t"; python tools/profile_search.py --m 8 16 32 64 --reps 3 --path 4 --tile $t 2>&1 | grep "rep=2" | awk "{print \$1, \$6, \$8, \$9}"; done > gpurun_out/exp.txt 2>&1
