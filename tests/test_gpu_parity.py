@@ -356,3 +356,23 @@ def test_prepare_batch_equals_prepare():
             h.close()
     with pytest.raises(hc.HCError):
         hc.prepare_batch([b"abc", b"a"], 2, 8)       # q > m for the second pattern
+
+
+@pytest.mark.parametrize("path", [hc.PATH_AUTO, hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC])
+def test_largest_tables_every_path(path):
+    """alpha = 15 (F = 128 KiB, the largest table) with short and long patterns on every
+    path: each either fits its shared-memory layout or falls back (stream -> gather);
+    SHC may refuse a layout it cannot fit (HC_EINVAL), never a failed launch."""
+    rng = np.random.default_rng(77)
+    y = I.gen_text("nl", 400_003, 77)
+    for m, q in [(6, 3), (20, 5), (40, 8), (150, 6)]:
+        o = int(rng.integers(0, len(y) - m))
+        x = y[o:o + m].copy()
+        want = oracle.brute(x, y)
+        h = hc.prepare(x, q, 15)
+        try:
+            got = gpu(h, to_dev(y, 2), path=path)
+        except hc.HCError as e:
+            assert path == hc.PATH_SHC and e.code == -1, (m, q, e)
+            continue
+        assert np.array_equal(got, want), (m, q)
