@@ -118,7 +118,9 @@ typedef struct hc_search_opts {
                          the TMA pipeline alone; 3 = phase A only; 6 = phase A on stale
                          stage data without waiting for TMA (filter compute alone); results
                          are NOT valid for debug != 0) */
-    int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage) */
+    int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage);
+                         stream: > 0 = each chunk by one 1-D TMA bulk copy instead of
+                         16-byte cp.async per lane */
     unsigned long long *trace; /* staged, debugging: DEVICE buffer of grid x trace_tiles x 4
                                   %globaltimer stamps per (CTA, tile), or NULL */
     int trace_tiles;

@@ -1155,7 +1155,8 @@ __host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m
     L.q2_off = L.q_off + nwarps * kStreamQ1 * 4u;
     L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
     L.ctr_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
-    L.buf_off = round_up(L.ctr_off + nwarps * 4u + 16, 128);
+    // per-warp counters, then 4 mbarriers per warp (TMA variant)
+    L.buf_off = round_up(round_up(L.ctr_off + nwarps * 4u, 8) + nwarps * 32u + 16, 128);
     L.total = L.buf_off + nwarps * bufs * buf_bytes;
     return L;
 }
@@ -1342,6 +1343,70 @@ __device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
     cp_async_wait<0>();
 }
 
+// The same loop with each chunk moved by ONE 1-D TMA bulk copy (cp.async.bulk, issued
+// by lane 0, completion on the buffer's mbarrier) instead of 16-byte cp.async per lane;
+// the partial 16-byte words at the two ends of an unaligned text are stored by the
+// lanes (first / last chunk only).
+template <int Q, int SH, int NB>
+__device__ __forceinline__ void stream_loop_tma(const KParams &p, const FTable &sF,
+                                                WarpQueueSink<Q, SH, GlobalText> &sink,
+                                                StreamQueue<Q, SH> &qu, uint32_t bufs0, uint64_t *bar,
+                                                uint32_t gw, uint32_t total_warps, uint32_t lane) {
+    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
+    const uintptr_t y = reinterpret_cast<uintptr_t>(p.y), ye = y + p.n;
+    if (lane == 0) {
+        for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](uint32_t c, uint32_t b) {
+        if (c >= p.nchunks) return;
+        const StreamChunk g = stream_chunk(p, c);
+        const uintptr_t A = (y + g.first) & ~static_cast<uintptr_t>(15);
+        const uint32_t nbytes =
+            static_cast<uint32_t>(((y + g.last + 16) & ~static_cast<uintptr_t>(15)) - A);
+        const uint32_t buf = bufs0 + b * p.stage_bytes;
+        const uintptr_t lo = max(A, (y + 15) & ~static_cast<uintptr_t>(15));
+        const uintptr_t hi = min(A + nbytes, ye & ~static_cast<uintptr_t>(15));
+        if (A < lo || A + nbytes > hi) {                 // edge chunk: bytes outside [lo, hi)
+            for (uintptr_t a = A + lane; a < A + nbytes; a += 32)
+                if ((a < lo || a >= hi) && a >= y && a < ye)
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + static_cast<uint32_t>(a - A)),
+                                 "r"(static_cast<uint32_t>(__ldg(reinterpret_cast<const uint8_t *>(a))))
+                                 : "memory");
+        }
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async();                         // earlier generic reads of the buffer
+            if (hi > lo) {
+                mbar_arrive_expect_tx(&bar[b], static_cast<uint32_t>(hi - lo));
+                bulk_g2s(buf + static_cast<uint32_t>(lo - A), reinterpret_cast<const void *>(lo),
+                         static_cast<uint32_t>(hi - lo), &bar[b]);
+            } else {
+                mbar_arrive(&bar[b]);
+            }
+        }
+    };
+#pragma unroll
+    for (int b = 0; b < NB - 1; ++b) issue(gw + b * total_warps, b);
+    uint32_t b = 0, par = 0;   // par: bit b = phase parity of buffer b's next completion
+    for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
+        const uint32_t bn = b == 0 ? NB - 1 : b - 1;
+        issue(c + (NB - 1) * total_warps, bn);
+        mbar_wait(&bar[b], (par >> b) & 1u);
+        par ^= 1u << b;
+        const StreamChunk g = stream_chunk(p, c);
+        const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
+        const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
+        if (p.debug != 1) {
+            stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+            qu.drain_all(sink, txt, lane);
+        }
+        __syncwarp();
+        b = b + 1 == NB ? 0 : b + 1;
+    }
+}
+
 template <int Q, int SH>
 __global__ void __launch_bounds__(kStreamMaxThreads) stream_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1368,7 +1433,13 @@ __global__ void __launch_bounds__(kStreamMaxThreads) stream_kernel(const KParams
     if (lane == 0) *ctr = 0;
     __syncwarp();
     StreamQueue<Q, SH> qu{reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kStreamQ1, ctr, 0u};
-    if (p.stages == 2)
+    if (p.tma_chunk) {
+        uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.ctr_off + round_up(NW * 4u, 8)) + warp * 4;
+        if (p.stages == 3)
+            stream_loop_tma<Q, SH, 3>(p, sF, sink, qu, bufs0, bar, gw, total_warps, lane);
+        else
+            stream_loop_tma<Q, SH, 2>(p, sF, sink, qu, bufs0, bar, gw, total_warps, lane);
+    } else if (p.stages == 2)
         stream_loop<Q, SH, 2>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
     else if (p.stages == 3)
         stream_loop<Q, SH, 3>(p, sF, sink, qu, bufs0, gw, total_warps, lane);

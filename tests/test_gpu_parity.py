@@ -376,3 +376,20 @@ def test_largest_tables_every_path(path):
             assert path == hc.PATH_SHC and e.code == -1, (m, q, e)
             continue
         assert np.array_equal(got, want), (m, q)
+
+
+def test_stream_tma_variant():
+    """The stream path with 1-D TMA bulk copies per chunk (opts.tma_chunk > 0):
+    unaligned texts, edge chunks, 2 and 3 buffers, against brute force."""
+    rng = np.random.default_rng(79)
+    for n in (1000, 70_001, 1_000_003):
+        y = I.gen_text("dna", n, 79 + n % 7)
+        for m, q in [(8, 4), (16, 6), (32, 6), (13, 2)]:
+            o = int(rng.integers(0, n - m))
+            x = y[o:o + m].copy()
+            want = oracle.brute(x, y)
+            for off in (0, 5, 15):
+                for stages in (2, 3):
+                    got = gpu(hc.prepare(x, q, 12), to_dev(y, off), path=hc.PATH_STREAM,
+                              tma_chunk=16, stages=stages)
+                    assert np.array_equal(got, want), (n, m, off, stages)
