@@ -1,1 +1,2 @@
-for r in 1 2; do for c in 0 16; do for d in 1 0; do echo "== tma=$c debug=$d"; python tools/profile_search.py --m 8 16 32 --reps 3 --path 3 --chunk $c --debug $d 2>&1 | grep -v "rep=0" | awk "{print \$1, \$5, \$6}"; done; done; done > gpurun_out/exp.txt 2>&1
+HC_LIB=build_obj/libhc_new.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2 > gpurun_out/parity.txt
+for r in 1 2; do for v in base new; do echo "== $v"; HC_LIB=build_obj/libhc_$v.so python tools/profile_search.py --m 8 16 32 64 1024 --reps 4 2>&1 | grep -v "rep=0" | awk "{print \$1, \$6}"; done; done > gpurun_out/exp.txt 2>&1
