@@ -240,6 +240,20 @@ def main():
     n = len(y_np)
     y = torch.from_numpy(y_np).to(dev)
     handles = [hc.prepare(x, q, a) for (m, q, a, o, x) in work]
+    # Preprocessing time per pattern (host Fig. 3 + upload; the paper times it with every
+    # search): hc_prepare alone, and amortised by hc_prepare_batch, per m
+    prep_us = {}
+    for m_ in cfg.ms:
+        xs_ = [x for (mm, q, a, o, x) in work if mm == m_]
+        qa_ = next((q, a) for (mm, q, a, o, x) in work if mm == m_)
+        t0 = time.perf_counter()
+        hs_ = [hc.prepare(x, *qa_) for x in xs_]
+        t1 = time.perf_counter()
+        hb_ = hc.prepare_batch(xs_, *qa_)
+        t2 = time.perf_counter()
+        for h_ in hs_ + hb_:
+            h_.close()
+        prep_us[m_] = (1e6 * (t1 - t0) / len(xs_), 1e6 * (t2 - t1) / len(xs_))
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush_buf = torch.ones(2 * l2, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize(dev)
@@ -405,6 +419,9 @@ def main():
             "pct_of_8TBps": round(100 * n / (med / 1e3) / 1e9 / 8000, 1),
             "q": d["q"], "alpha": d["alpha"], "path": d["path"],
             "occ_per_pattern": round(d["occ"] / len(d["t"]) * args.steps, 2),
+            "prepare_us": round(prep_us[m][0], 2),
+            "prepare_batch_us_per_pattern": round(prep_us[m][1], 2),
+            "GBps_incl_prepare": round(n / ((med + prep_us[m][0] / 1e3) / 1e3) / 1e9, 1),
         }
         if use_batch:
             bms = [bt[m] for bt in all_batch]
