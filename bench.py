@@ -331,6 +331,7 @@ def main():
 
     def batch_step(timed: bool):
         tms = {}
+        nl = 0
         for m, idx in by_m.items():
             flush_l2()
             got = hc.search_batch_raw([handles[k] for k in idx], y.data_ptr(), n,
@@ -338,7 +339,8 @@ def main():
                                       opts, bst)
             assert got == [counts[k] for k in idx], m
             tms[m] = bst.kernel_ms
-        return tms, 2 * len(work)
+            nl += bst.launches          # search (single or multi-pattern) + finish kernels
+        return tms, nl
 
     for _ in range(args.warmup):
         step(False)
