@@ -109,7 +109,7 @@ typedef struct hc_search_opts {
     int path;         /* hc_path */
     int tile_bytes;   /* staged: text bytes per shared-memory stage; stream: target text bytes
                          per warp chunk (0 = default) */
-    int stages;       /* staged: TMA pipeline depth; stream: buffers per warp, 2..4 (0 = default) */
+    int stages;       /* staged: TMA pipeline depth; stream: buffers per warp, 2..4 (0 = default 2) */
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
     int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms) */
@@ -149,10 +149,14 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
 
 /* Batch of independent searches over the same text (multi-pattern
  * batching): the result of pattern i is exactly hc_search(hs[i], y_dev, n, pos_out[i],
- * max_out[i], stream) (Fig. 5, per pattern).  The searches are spread over
- * a few library-owned streams so that one pattern's tail and launch latency overlap
- * the next pattern's work; the call is ordered after prior work on `stream`, and
- * returns after all of them completed (stream order is preserved for later work).
+ * max_out[i], stream) (Fig. 5, per pattern).  Consecutive patterns of
+ * equal (m, q, alpha) with shifts m - q + 1 <= 256 are searched up to 4 per launch by
+ * the multi-pattern kernel: one pass over the text, each lattice q-gram hashed once
+ * and tested against every pattern's F (opts->no_multi = 1 disables it).  Launches
+ * are spread over 8 library-owned streams so that one launch's tail and launch
+ * latency overlap the next one's work; the call is ordered after prior work on
+ * `stream`, and returns after all of them completed (stream order is preserved for
+ * later work).
  *   hs      : npat handles (same device), read-only.
  *   y_dev   : DEVICE text, n bytes, caller-owned, read-only.
  *   counts  : HOST int64[npat], receives each pattern's occurrence count.
