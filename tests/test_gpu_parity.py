@@ -63,7 +63,7 @@ def test_random_small(path):
         sigma = int(rng.choice([2, 4, 20, 64, 256]))
         q = int(rng.integers(1, 9))
         m = int(rng.integers(q, 140))
-        alpha = int(rng.integers(8, 13))
+        alpha = int(rng.integers(1, 16))
         n = int(rng.integers(0, 60_000))
         y = rng.integers(0, sigma, n, dtype=np.uint8)
         if n >= m and rng.random() < 0.8:
@@ -376,6 +376,82 @@ def test_largest_tables_every_path(path):
             assert path == hc.PATH_SHC and e.code == -1, (m, q, e)
             continue
         assert np.array_equal(got, want), (m, q)
+
+
+def _all_qs_builds():
+    """Every (q, s) kernel build the ABI can reach: 1 <= q <= 8, 1 <= alpha <= 15,
+    s = floor(alpha / q) (Eq. 4; s = 0 when q > alpha, reading R6).  For q = 1
+    the hash is the byte itself (one build, s plays no role)."""
+    builds = {}
+    for q in range(1, 9):
+        for alpha in range(1, 16):
+            key = (q, 0 if q == 1 else alpha // q)
+            builds.setdefault(key, []).append(alpha)
+    return builds
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_every_kernel_build(path):
+    """Every (q, s) instantiation, every alpha in 1..15 (the scalar F-load branch at
+    alpha <= 1, s = 0 at q > alpha), short and long patterns (m = q, m < 2q for the
+    while-else of R7, walks of several steps, m > 64 for the warp-wide verification),
+    planted occurrences, unaligned text: element-wise equal to brute force (O1)."""
+    builds = _all_qs_builds()
+    assert len(builds) == 31
+    rng = np.random.default_rng(81 + path)
+    seen = set()
+    for (q, s), alphas in sorted(builds.items()):
+        for alpha in alphas:
+            sigma = int(rng.choice([2, 4, 20, 256]))
+            y = rng.integers(0, sigma, int(rng.integers(20_000, 40_000)), dtype=np.uint8)
+            for m in sorted({q, q + 1, 2 * q - 1 if q > 1 else 1, 2 * q + 3, 37, 150}):
+                if m < q:
+                    continue
+                o = int(rng.integers(0, len(y) - m))
+                x = y[o:o + m].copy()
+                yy = y.copy()
+                for p in rng.integers(0, len(y) - m, 6):
+                    yy[p:p + m] = x
+                want = oracle.brute(x, yy)
+                h = hc.prepare(x, q, alpha)
+                t = h.table()
+                assert t.s == (alpha // q)
+                off = int(rng.integers(0, 16))
+                try:
+                    got = gpu(h, to_dev(yy, off), path=path)
+                except hc.HCError as e:        # SHC may refuse a layout it cannot fit
+                    assert path == hc.PATH_SHC and e.code == hc.HC_EINVAL, (q, alpha, m, e)
+                    continue
+                assert np.array_equal(got, want), (q, s, alpha, m, off, len(got), len(want))
+                seen.add((q, s))
+    assert seen == set(builds), sorted(set(builds) - seen)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_long_patterns(path):
+    """m in the thousands (warp-wide walks of hundreds of steps, 1 KiB verification
+    rounds) and m = HC_MAX_PATTERN = 65536: the default path must search exactly; a
+    forced path either searches exactly or refuses the layout with HC_EINVAL."""
+    rng = np.random.default_rng(83)
+    y = I.gen_text("protein", 600_011, 83)
+    for m, q, alpha in [(4099, 4, 12), (8000, 6, 12), (12_345, 3, 11), (16_000, 8, 15), (65_536, 4, 12)]:
+        o = int(rng.integers(0, len(y) - m))
+        x = y[o:o + m].copy()
+        yy = y.copy()
+        for p in rng.integers(0, len(y) - m, 3):
+            yy[p:p + m] = x
+        yy[o + m // 2] ^= 1 if rng.random() < 0.5 else 0     # sometimes a near-miss at o
+        want = oracle.brute(x, yy)
+        h = hc.prepare(x, q, alpha)
+        try:
+            got = gpu(h, to_dev(yy, 7), path=path)
+        except hc.HCError as e:
+            assert path in (hc.PATH_SHC, hc.PATH_STAGED) and e.code == hc.HC_EINVAL, (m, e)
+            continue
+        assert np.array_equal(got, want), (m, q, alpha, len(got), len(want))
+    with pytest.raises(hc.HCError) as ei:
+        hc.prepare(bytes(65_537), 4, 12)
+    assert ei.value.code == hc.HC_ETOOLONG
 
 
 def test_stream_tma_variant():
