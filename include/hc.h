@@ -114,15 +114,15 @@ typedef struct hc_search_opts {
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
     int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms) */
     int ctas_per_sm;  /* cap on resident CTAs per SM for the persistent grid (0 = occupancy max) */
-    int debug;        /* 0; 1 = staged path streams the tiles but skips the search (measures
-                         the TMA pipeline alone; 3 = phase A only; 6 = phase A on stale
-                         stage data without waiting for TMA (filter compute alone); results
-                         are NOT valid for debug != 0) */
+    int debug;        /* must be 0.  Measurement-only modes (1 = copy pipeline alone, 3 = phase A
+                         only, 5 = phase-B counters, 6 = filter on stale stage data; results NOT
+                         valid) exist only in the instrumented build libhc_instr.so
+                         (HC_INSTRUMENT=1, tools/); this library returns HC_EINVAL if set */
     int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage);
                          stream: > 0 = each chunk by one 1-D TMA bulk copy instead of
                          16-byte cp.async per lane */
-    unsigned long long *trace; /* staged, debugging: DEVICE buffer of grid x trace_tiles x 4
-                                  %globaltimer stamps per (CTA, tile), or NULL */
+    unsigned long long *trace; /* must be NULL (instrumented build only: DEVICE buffer of
+                                  grid x trace_tiles x 4 %globaltimer stamps per (CTA, tile)) */
     int trace_tiles;
     int surv_warps;   /* staged: survivor/producer warps per CTA (0 = default) */
     int block_warps;  /* stream: warps per CTA, 1..8 (0 = default 8) */
@@ -139,7 +139,7 @@ typedef struct hc_search_stats {
     int reruns;        /* search re-runs after the position scratch overflowed */
     float kernel_ms;   /* if time_kernel: device time from the search launch to the end of the
                           call's last kernel (search + result ordering), first attempt */
-    uint32_t dbg[2];   /* debug == 5: phase-B loop iterations and phase-B calls */
+    uint32_t dbg[2];   /* instrumented build, debug == 5: phase-B loop iterations and calls */
 } hc_search_stats;
 
 /* hc_search with explicit options (NULL = defaults) and optional statistics (NULL = none). */

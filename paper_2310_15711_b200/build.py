@@ -18,8 +18,13 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhc.so")
-SOURCES = ["hc_api.cpp", "hc_kernels.cu"]
-HEADERS = ["hc_internal.h"]
+# instrumented build (HC_INSTRUMENT=1): opts.debug modes and %globaltimer traces compiled
+# in, for tools/ only; the product library rejects them (HC_EINVAL)
+LIB_INSTR = os.path.join(HERE, "libhc_instr.so")
+OBJ = os.path.join(ROOT, "build_obj")
+SOURCES = ["hc_api.cpp", "hc_launch.cu", "hc_stream.cu", "hc_gather.cu", "hc_mstream.cu",
+           "hc_finish.cu", "hc_shc.cu", "hc_staged.cu"]
+HEADERS = ["hc_internal.h", "hc_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -30,26 +35,40 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found (CUDA 12.9 toolkit required)")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "hc.h"),
                                                                  __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+def _compile(src: str, obj: str, defs: list, verbose: bool) -> None:
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-           "-Xptxas", "-v" if verbose else "-O3", "-shared", "-I", INCLUDE, "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+           "-Xptxas", "-v" if verbose else "-O3", *defs, "-I", INCLUDE, "-I", CSRC,
+           "-c", os.path.join(CSRC, src), "-o", obj]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+
+
+def build(force: bool = False, verbose: bool = False, instrument: bool = False) -> str:
+    """Compiles every translation unit (in parallel) and links the shared library."""
+    lib = LIB_INSTR if instrument else LIB
+    if not force and not _stale(lib):
+        return lib
+    from concurrent.futures import ThreadPoolExecutor
+    tag = "instr" if instrument else "prod"
+    os.makedirs(os.path.join(OBJ, tag), exist_ok=True)
+    defs = [f"-DHC_INSTRUMENT={1 if instrument else 0}"]
+    objs = [os.path.join(OBJ, tag, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda so: _compile(so[0], so[1], defs, verbose), zip(SOURCES, objs)))
+    tmp = lib + f".tmp{os.getpid()}"
+    subprocess.check_call([nvcc(), *ARCH, "-shared", *objs, "-o", tmp])
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                instrument="--instrument" in sys.argv))

@@ -1,7 +1,7 @@
 // hc_api.cpp — host side of libhc: the C-ABI of include/hc.h.
 //
 //   hc_prepare     Preprocessing (Fig. 3) on the host + upload of F and x.
-//   hc_search(_ex) validation, path choice, search kernel launch (hc_kernels.cu),
+//   hc_search(_ex) validation, path choice, search kernel launch (hc_*.cu),
 //                  count read-back, position ordering.
 //
 // The table build below is this library's own implementation of Fig. 3: it
@@ -24,6 +24,10 @@
 
 #include "hc.h"
 #include "hc_internal.h"
+
+#ifndef HC_INSTRUMENT
+#define HC_INSTRUMENT 0
+#endif
 
 struct hc_handle {
     std::vector<uint8_t> x;
@@ -84,8 +88,9 @@ void build_table(const uint8_t *x, uint32_t m, uint32_t q, uint32_t alpha, uint3
 // Per-host-thread, per-device scratch: [counter (16 B) | positions (cap u32)] plus a
 // mapped pinned word the finish kernel writes the count into.  hc_search returns only
 // after all of its device work completed, so the next call on this thread (any
-// stream) can reuse it; the counter is zeroed once here and reset by every finish
-// kernel afterwards.
+// stream) can reuse it.  A new buffer's counter is zeroed by cudaMemsetAsync on the
+// stream that will use it (a plain cudaMemset runs on the legacy stream, which a
+// non-blocking caller stream does not wait for), and every finish kernel resets it.
 struct Scratch {
     int dev = -1;
     uint32_t *buf = nullptr;       // device
@@ -95,7 +100,7 @@ struct Scratch {
 };
 thread_local Scratch g_scratch[8];
 
-cudaError_t get_scratch(int dev, size_t cap, Scratch **out) {
+cudaError_t get_scratch(int dev, size_t cap, cudaStream_t st, Scratch **out) {
     if (dev < 0 || dev >= 8) return cudaErrorInvalidDevice;
     Scratch &sc = g_scratch[dev];
     if (!sc.host_count) {
@@ -117,7 +122,7 @@ cudaError_t get_scratch(int dev, size_t cap, Scratch **out) {
             sc.cap = 0;
             return e;
         }
-        e = cudaMemset(sc.buf, 0, 16);
+        e = cudaMemsetAsync(sc.buf, 0, 16, st);
         if (e != cudaSuccess) return e;
         sc.cap = want;
     }
@@ -326,7 +331,7 @@ thread_local BatchRes g_batch[8];
 // Batch scratch of one pool stream: [kMaxPatterns counters of 16 B | positions], the
 // positions of a multi-pattern launch's pattern g at offset g * (cap / npat).
 constexpr size_t kCtrWords = 4 * hc::kMaxPatterns;
-cudaError_t batch_scratch(Scratch &sc, size_t cap) {
+cudaError_t batch_scratch(Scratch &sc, size_t cap, cudaStream_t st) {
     if (!sc.buf || sc.cap < cap) {
         if (sc.buf) cudaFree(sc.buf);
         sc.buf = nullptr;
@@ -335,7 +340,7 @@ cudaError_t batch_scratch(Scratch &sc, size_t cap) {
             sc.cap = 0;
             return e;
         }
-        e = cudaMemset(sc.buf, 0, kCtrWords * sizeof(uint32_t));
+        e = cudaMemsetAsync(sc.buf, 0, kCtrWords * sizeof(uint32_t), st);   // on the user stream
         if (e != cudaSuccess) return e;
         sc.cap = cap;
     }
@@ -568,6 +573,8 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     if (n > HC_MAX_TEXT) return fail(HC_ETOOLONG);
     hc_search_opts o{};
     if (opts) o = *opts;
+    if (!HC_INSTRUMENT && (o.debug != 0 || o.trace != nullptr))
+        return fail(HC_EINVAL);   // measurement-only modes exist in libhc_instr.so only
     if (stats) *stats = hc_search_stats{};
     g_last_error = HC_OK;
     if (n < h->m) return 0;  // S:123, reading R9
@@ -599,7 +606,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     hc::LaunchInfo li;
     for (int attempt = 0;; ++attempt) {
         Scratch *sc = nullptr;
-        cudaError_t e = get_scratch(h->device, cap, &sc);
+        cudaError_t e = get_scratch(h->device, cap, stream, &sc);
         if (e != cudaSuccess) return cuda_fail(e, "scratch");
         p.counter = sc->buf;
         p.out = want_pos ? sc->buf + 4 : nullptr;
@@ -644,7 +651,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             return cuda_fail(e, stage);
         }
         count = *reinterpret_cast<volatile uint32_t *>(sc->host_count);
-        if (o.debug == 5 && stats) {
+        if (HC_INSTRUMENT && o.debug == 5 && stats) {
             cudaMemcpy(stats->dbg, sc->buf + 2, 8, cudaMemcpyDeviceToHost);
             cudaMemset(sc->buf + 2, 0, 8);
         }
@@ -717,6 +724,30 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
     cudaEventRecord(r->ev[kBatchStreams], stream);
     for (int j = 0; j < kBatchStreams; ++j) cudaStreamWaitEvent(r->st[j], r->ev[kBatchStreams], 0);
 
+    // One exit for every failure after this point: the caller's stream waits for the
+    // pool streams (launches already queued keep writing r->hcounts and the scratch),
+    // everything is synchronised, the events are destroyed, and the pool scratch is
+    // dropped (its counters may be left non-zero).  Only then is the error returned.
+    auto join_pool = [&]() {
+        for (int j = 0; j < kBatchStreams; ++j) {
+            cudaEventRecord(r->ev[j], r->st[j]);
+            cudaStreamWaitEvent(stream, r->ev[j], 0);
+        }
+    };
+    auto bail = [&](int code) -> int {
+        join_pool();
+        cudaStreamSynchronize(stream);
+        cudaGetLastError();
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        for (int j = 0; j < kBatchStreams; ++j) {
+            if (r->sc[j].buf) cudaFree(r->sc[j].buf);
+            r->sc[j].buf = nullptr;
+            r->sc[j].cap = 0;
+        }
+        return code;
+    };
+
     std::vector<size_t> caps(npat, 0);
     int launches = 0;
     int nlaunch = 0;   // search launches so far (round-robin over the pool streams)
@@ -755,7 +786,7 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
             for (; g > 1; --g) {
                 og.tile_bytes = stream_multi && o.tile_bytes == 0 && g > 2 ? 2048 : o.tile_bytes;
                 const int rc = setup_search(h, y_dev, nn, og, p, path);
-                if (rc != HC_OK) return fail(rc);
+                if (rc != HC_OK) return fail(bail(rc));
                 if (path != multi_path) continue;
                 if (stream_multi) {
                     p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
@@ -776,7 +807,7 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
         }
         if (g == 1) {
             const int rc = setup_search(h, y_dev, nn, o, p, path);
-            if (rc != HC_OK) return fail(rc);
+            if (rc != HC_OK) return fail(bail(rc));
         }
         // per-pattern position capacity
         size_t cap = 0;
@@ -785,8 +816,8 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
             if (pos_out && pos_out[i + t] && mo > 0)
                 cap = std::max(cap, std::min<size_t>(std::max<size_t>(mo, size_t(1) << 16), windows));
         }
-        e = batch_scratch(sc, std::max<size_t>(cap * g, 1));
-        if (e != cudaSuccess) return cuda_fail(e, "batch scratch");
+        e = batch_scratch(sc, std::max<size_t>(cap * g, 1), r->st[j]);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "batch scratch"));
         hc::LaunchInfo li;
         if (g == 1) {
             const size_t mo = max_out ? max_out[i] : 0;
@@ -825,31 +856,15 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
                                   p.n, r->hcounts_dev + i + t, r->st[j]);
             ++launches;
         }
-        if (e != cudaSuccess) return cuda_fail(e, "batch launch");
+        if (e != cudaSuccess) return bail(cuda_fail(e, "batch launch"));
         i += g;
     }
-    for (int j = 0; j < kBatchStreams; ++j) {
-        cudaEventRecord(r->ev[j], r->st[j]);
-        cudaStreamWaitEvent(stream, r->ev[j], 0);
-    }
-    if (o.time_kernel) cudaEventRecord(ev1, stream);
+    join_pool();
     e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) {
-        for (int j = 0; j < kBatchStreams; ++j) {   // counters may be left non-zero
-            cudaFree(r->sc[j].buf);
-            r->sc[j].buf = nullptr;
-            r->sc[j].cap = 0;
-        }
-        return cuda_fail(e, "batch execution");
-    }
-    float kms = 0.f;
-    if (o.time_kernel) {
-        cudaEventElapsedTime(&kms, ev0, ev1);
-        cudaEventDestroy(ev0);
-        cudaEventDestroy(ev1);
-    }
-    // patterns whose positions did not fit the scratch or need the large sort are run
-    // again on their own (their counts are exact already)
+    if (e != cudaSuccess) return bail(cuda_fail(e, "batch execution"));
+    // patterns whose positions did not fit the scratch or need the large ordering are run
+    // again on their own (their counts are exact already); the device time of the batch
+    // (stats->kernel_ms) runs to the end of these re-runs
     int reruns = 0;
     for (size_t i = 0; i < npat; ++i) {
         const uint32_t c = reinterpret_cast<volatile uint32_t *>(r->hcounts)[i];
@@ -857,11 +872,22 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
         const size_t mo = max_out ? max_out[i] : 0;
         const bool want_pos = pos_out && pos_out[i] && mo > 0;
         if (want_pos && c > 0 && (c > caps[i] || c > hc::kSmallSort)) {
-            const int64_t c2 = hc_search_ex(hs[i], y_dev, n, pos_out[i], mo, stream, &o, nullptr);
-            if (c2 < 0) return static_cast<int>(c2);
+            hc_search_opts orr = o;
+            orr.time_kernel = 0;
+            hc_search_stats rs{};
+            const int64_t c2 = hc_search_ex(hs[i], y_dev, n, pos_out[i], mo, stream, &orr, &rs);
+            if (c2 < 0) return bail(static_cast<int>(c2));
+            launches += rs.launches;
             counts[i] = c2;
             ++reruns;
         }
+    }
+    float kms = 0.f;
+    if (o.time_kernel) {
+        cudaEventRecord(ev1, stream);
+        if (cudaEventSynchronize(ev1) == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
     }
     if (stats) {
         stats->launches = launches;

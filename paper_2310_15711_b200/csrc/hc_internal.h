@@ -1,5 +1,5 @@
 // Internal interface between the host side (hc_api.cpp) and the device side
-// (hc_kernels.cu) of libhc.  Not part of the C-ABI.
+// (hc_*.cu, one translation unit per search path) of libhc.  Not part of the C-ABI.
 #pragma once
 
 #include <cstddef>
@@ -58,7 +58,7 @@ struct LaunchInfo {
     int grid = 0, block = 0, smem = 0;
 };
 
-// Device-side entry points (hc_kernels.cu).  All enqueue on `st`.
+// Device-side entry points (hc_stream.cu, hc_gather.cu, ...).  All enqueue on `st`.
 cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
 cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,

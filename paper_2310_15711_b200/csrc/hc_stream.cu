@@ -1,0 +1,280 @@
+// hc_stream.cu — stream path (HC_PATH_STREAM, the default for shifts S <= 32):
+// per-warp chunks staged in shared memory by 16-byte cp.async copies (or one 1-D TMA
+// bulk copy per chunk, opts.tma_chunk), lattice filter on the stage, survivors through
+// first steps on the stage and phase B on global text.  DESIGN.md 5.
+#include "hc_device.cuh"
+
+namespace hc {
+
+// ------------------------------------------------------------------ stream kernel
+// Small shifts (S <= 32), every text sector is read (f(m) = 1).  Each warp
+// owns a contiguous run of segments per chunk and stages exactly the chunk's lattice
+// q-gram bytes [k0 S + S - 1, k1 S + q - 2] into its own shared-memory buffer with
+// 16-byte cp.async copies (coalesced, L2-only), kStreamBufs - 1 chunks ahead of the
+// one it filters: no CTA-wide barrier, no hand-off between warps.  Phase A reads the
+// buffer; the lattice survivors go through first_steps and phase B on global text
+// (the chunk was just streamed through L2), exactly as on the gather path.
+struct StreamLayout {
+    uint32_t f_off, x_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
+};
+__host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m, uint32_t nwarps,
+                                                      uint32_t buf_bytes, uint32_t bufs) {
+    StreamLayout L;
+    L.f_off = 0;
+    L.x_off = round_up((1u << alpha) * 4u, 16);
+    L.q_off = L.x_off + round_up(m + 8, 16);
+    L.q2_off = L.q_off + nwarps * kStreamQ1 * 4u;
+    L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
+    L.ctr_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    // per-warp counters, then 4 mbarriers per warp (TMA variant)
+    L.buf_off = round_up(round_up(L.ctr_off + nwarps * 4u, 8) + nwarps * 32u + 16, 128);
+    L.total = L.buf_off + nwarps * bufs * buf_bytes;
+    return L;
+}
+int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs,
+                      uint32_t nwarps) {
+    return static_cast<int>(stream_layout(alpha, m, nwarps, buf_bytes, bufs).total);
+}
+
+// Phase A of the stream path over lattice points [k0, k1) of a staged chunk: the same
+// l.4-6 test as filter_lattice, but the survivors are appended to a per-warp queue
+// (q1, count n1, shared slot counter ctr) with one shared atomic per lane that has
+// any, and the queue is drained (first_steps, phase B: calls) only between runs of
+// trips, so the trip loop has no call in it and keeps its state in registers.
+template <int Q, int SH>
+struct StreamQueue {
+    uint32_t *q1;     // kStreamQ1 window ends a_k
+    uint32_t *ctr;    // shared slot counter (= n1 between trips)
+    uint32_t n1;      // warp-uniform count
+    // first steps of 32 queued survivors, on the chunk's stage (the queue only ever
+    // holds survivors of the chunk being filtered: it is drained at the chunk's end)
+    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText> &sink,
+                                            const SmemText &txt, uint32_t lane) {
+        __syncwarp();
+        const uint32_t e = q1[n1 - 32 + lane];
+        n1 -= 32;
+        __syncwarp();
+        if (lane == 0) *ctr = n1;
+        __syncwarp();
+        sink.steps_e_on(txt, true, e);
+    }
+    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText> &sink,
+                                              const SmemText &txt, uint32_t lane) {
+        while (n1 >= 32) drain32(sink, txt, lane);
+        if (n1) {
+            __syncwarp();
+            const bool act = lane < n1;
+            const uint32_t e = act ? q1[lane] : 0u;
+            n1 = 0;
+            __syncwarp();
+            if (lane == 0) *ctr = 0;
+            __syncwarp();
+            sink.steps_e_on(txt, act, e);
+        }
+    }
+};
+
+template <int Q, int SH>
+__device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &txt, const FTable &sF,
+                                              uint32_t k0, uint32_t k1, uint32_t lane,
+                                              StreamQueue<Q, SH> &qu,
+                                              WarpQueueSink<Q, SH, GlobalText> &sink) {
+    const uint32_t step = 32 * p.S;
+    uint32_t pos = p.m - 1 + (k0 + lane) * p.S;   // window end a_k of lattice point k0 + lane
+    uint32_t k = k0;
+    while (true) {
+        while (k + 32 * kStreamUnroll <= k1 && qu.n1 < 32) {
+            uint64_t W[kStreamUnroll];
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
+            uint32_t pm = 0;
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u)
+                pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
+            if (kInstrument && p.debug == 3) pm = 0;   // phase A alone (measurement)
+            const uint32_t c = __popc(pm);
+            const uint32_t tot = __reduce_add_sync(HC_FULL, c);
+            if (tot) {
+                if (c) {
+                    uint32_t slot = atomicAdd(qu.ctr, c);
+#pragma unroll
+                    for (int u = 0; u < kStreamUnroll; ++u)
+                        if ((pm >> u) & 1u) qu.q1[slot++] = pos + u * step;
+                }
+                qu.n1 += tot;
+            }
+            k += 32 * kStreamUnroll;
+            pos += kStreamUnroll * step;
+        }
+        if (qu.n1 < 32) break;
+        qu.drain32(sink, txt, lane);
+    }
+    for (; k < k1; k += 32, pos += step) {          // ragged tail, one round at a time
+        const bool in = k + lane < k1;
+        const bool pass = in && sF.pass(qhash<Q, SH>(end8<Q>(txt, pos), p.mask));
+        const uint32_t bm = __ballot_sync(HC_FULL, pass);
+        if (bm) {
+            if (pass) qu.q1[qu.n1 + __popc(bm & lanemask_lt())] = pos;
+            qu.n1 += __popc(bm);
+            __syncwarp();
+            if (lane == 0) *qu.ctr = qu.n1;
+            if (qu.n1 >= 32) qu.drain32(sink, txt, lane);
+        }
+    }
+}
+
+template <int Q, int SH, int NB>
+__device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
+                                            WarpQueueSink<Q, SH, GlobalText> &sink,
+                                            StreamQueue<Q, SH> &qu, uint32_t bufs0,
+                                            uint32_t gw, uint32_t total_warps, uint32_t lane) {
+    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
+#pragma unroll
+    for (int b = 0; b < NB - 1; ++b) stream_issue(p, gw + b * total_warps, bufs0 + b * p.stage_bytes, lane);
+    uint32_t b = 0;
+    for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
+        // refill the buffer filtered last round with the chunk NB-1 ahead
+        const uint32_t bn = b == 0 ? NB - 1 : b - 1;
+        stream_issue(p, c + (NB - 1) * total_warps, bufs0 + bn * p.stage_bytes, lane);
+        cp_async_wait<NB - 1>();   // chunk c's group is complete (this lane's copies)
+        __syncwarp();              // ... and every lane's, visible to the warp
+        const StreamChunk g = stream_chunk(p, c);
+        const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
+        const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
+        if (!(kInstrument && p.debug == 1)) {   // debug 1: copy pipeline alone
+            stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+            qu.drain_all(sink, txt, lane);
+        }
+        __syncwarp();              // every lane is done with buffer b before its refill
+        b = b + 1 == NB ? 0 : b + 1;
+    }
+    cp_async_wait<0>();
+}
+
+// The same loop with each chunk moved by ONE 1-D TMA bulk copy (cp.async.bulk, issued
+// by lane 0, completion on the buffer's mbarrier) instead of 16-byte cp.async per lane;
+// the partial 16-byte words at the two ends of an unaligned text are stored by the
+// lanes (first / last chunk only).
+template <int Q, int SH, int NB>
+__device__ __forceinline__ void stream_loop_tma(const KParams &p, const FTable &sF,
+                                                WarpQueueSink<Q, SH, GlobalText> &sink,
+                                                StreamQueue<Q, SH> &qu, uint32_t bufs0, uint64_t *bar,
+                                                uint32_t gw, uint32_t total_warps, uint32_t lane) {
+    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
+    const uintptr_t y = reinterpret_cast<uintptr_t>(p.y), ye = y + p.n;
+    if (lane == 0) {
+        for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](uint32_t c, uint32_t b) {
+        if (c >= p.nchunks) return;
+        const StreamChunk g = stream_chunk(p, c);
+        const uintptr_t A = (y + g.first) & ~static_cast<uintptr_t>(15);
+        const uint32_t nbytes =
+            static_cast<uint32_t>(((y + g.last + 16) & ~static_cast<uintptr_t>(15)) - A);
+        const uint32_t buf = bufs0 + b * p.stage_bytes;
+        const uintptr_t lo = max(A, (y + 15) & ~static_cast<uintptr_t>(15));
+        const uintptr_t hi = min(A + nbytes, ye & ~static_cast<uintptr_t>(15));
+        if (A < lo || A + nbytes > hi) {                 // edge chunk: bytes outside [lo, hi)
+            for (uintptr_t a = A + lane; a < A + nbytes; a += 32)
+                if ((a < lo || a >= hi) && a >= y && a < ye)
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + static_cast<uint32_t>(a - A)),
+                                 "r"(static_cast<uint32_t>(__ldg(reinterpret_cast<const uint8_t *>(a))))
+                                 : "memory");
+        }
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async();                         // earlier generic reads of the buffer
+            if (hi > lo) {
+                mbar_arrive_expect_tx(&bar[b], static_cast<uint32_t>(hi - lo));
+                bulk_g2s(buf + static_cast<uint32_t>(lo - A), reinterpret_cast<const void *>(lo),
+                         static_cast<uint32_t>(hi - lo), &bar[b]);
+            } else {
+                mbar_arrive(&bar[b]);
+            }
+        }
+    };
+#pragma unroll
+    for (int b = 0; b < NB - 1; ++b) issue(gw + b * total_warps, b);
+    uint32_t b = 0, par = 0;   // par: bit b = phase parity of buffer b's next completion
+    for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
+        const uint32_t bn = b == 0 ? NB - 1 : b - 1;
+        issue(c + (NB - 1) * total_warps, bn);
+        mbar_wait(&bar[b], (par >> b) & 1u);
+        par ^= 1u << b;
+        const StreamChunk g = stream_chunk(p, c);
+        const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
+        const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
+        if (!(kInstrument && p.debug == 1)) {   // debug 1: copy pipeline alone
+            stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+            qu.drain_all(sink, txt, lane);
+        }
+        __syncwarp();
+        b = b + 1 == NB ? 0 : b + 1;
+    }
+}
+
+template <int Q, int SH>
+__global__ void __launch_bounds__(kStreamMaxThreads) stream_kernel(const KParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t NW = blockDim.x / 32;
+    const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages);
+    uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
+    uint8_t *sx = smem + L.x_off;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (kInstrument && tid == 0) trace_cta(p, 0);
+    pdl_launch_dependents();
+    const uint32_t total_warps = gridDim.x * NW;
+    const uint32_t gw = blockIdx.x * NW + warp;
+    const uint32_t bufs0 = smem_u32(smem + L.buf_off) + warp * p.stages * p.stage_bytes;
+    load_table(p, sFp, sx);
+    if (tid == 0) s_params[0] = p;
+    __syncthreads();
+    const FTable sF{fence_value(smem_u32(sFp))};
+    WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
+    const GlobalText gtxt{p.y};
+    WarpQueueSink<Q, SH, GlobalText> sink{p, gtxt, sF, sx, nullptr,
+                                          reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
+                                          0u, 0u, wo, lane};
+    uint32_t *ctr = reinterpret_cast<uint32_t *>(smem + L.ctr_off) + warp;
+    if (lane == 0) *ctr = 0;
+    __syncwarp();
+    StreamQueue<Q, SH> qu{reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kStreamQ1, ctr, 0u};
+    if (p.tma_chunk) {
+        uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.ctr_off + round_up(NW * 4u, 8)) + warp * 4;
+        if (p.stages == 3)
+            stream_loop_tma<Q, SH, 3>(p, sF, sink, qu, bufs0, bar, gw, total_warps, lane);
+        else
+            stream_loop_tma<Q, SH, 2>(p, sF, sink, qu, bufs0, bar, gw, total_warps, lane);
+    } else if (p.stages == 2)
+        stream_loop<Q, SH, 2>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    else if (p.stages == 3)
+        stream_loop<Q, SH, 3>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    else
+        stream_loop<Q, SH, 4>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    sink.drain();
+    wo.flush(p, lane);
+    if (kInstrument && lane == 0) trace_cta(p, 1);
+}
+
+template <int Q, int SH>
+struct PickStream {
+    using Fn = KernFn;
+    static KernFn fn() { return stream_kernel<Q, SH>; }
+};
+
+cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                          LaunchInfo *li) {
+    KernFn kern = pick<PickStream>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
+    const uint32_t nw = p.block_warps;
+    const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, nw);
+    const long ctas = (p.nchunks + nw - 1) / nw;
+    KParams a = p;
+    void *args[] = {&a};
+    return launch_kernel(reinterpret_cast<const void *>(kern), args, static_cast<int>(32 * nw), smem,
+                         ctas, max_ctas, ctas_per_sm, st, li);
+}
+
+}  // namespace hc

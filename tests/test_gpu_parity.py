@@ -169,6 +169,12 @@ def test_errors():
         hc.search_raw(h, 0, 100, None, 0, 0)
     assert ei.value.code == hc.HC_EINVAL
     assert hc.search_raw(h, 0, 0, None, 0, 0) == 0          # n = 0 -> 0
+    # measurement-only modes are compiled out of the product library
+    y = to_dev(np.frombuffer(b"xxabcdxx", np.uint8))
+    for kw in ({"debug": 3}, {"trace": 8}):
+        with pytest.raises(hc.HCError) as ei:
+            hc.search(h, y, **kw)
+        assert ei.value.code == hc.HC_EINVAL
     with pytest.raises(hc.HCError):
         hc.prepare(b"ab", 3, 8)
 

@@ -12,6 +12,10 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+if any(a.startswith("--debug") for a in sys.argv) or "--trace" in sys.argv:
+    # measurement-only modes exist in the instrumented build only (HC_INSTRUMENT=1)
+    from paper_2310_15711_b200 import build as _b
+    os.environ["HC_LIB"] = _b.build(instrument=True)
 from paper_2310_15711_b200 import hc  # noqa: E402
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
