@@ -7,13 +7,18 @@ searched per pattern vs m on 1 B200, % of HBM peak; bit-exact).
 Workload (N=1): BASELINE.json configs[1] = C2, DNA-like i.i.d. text of 256 MiB,
 m in {8,...,1024}, 100 patterns per m copied from seeded text offsets, (q, alpha)
 per m from the paper's Table 1 (inputs.py).  One STEP searches every (m, pattern)
-of the config once (the whole hot path: search kernel, count read-back, ordering of
-the positions into the caller's int64 buffer), i.e. 800 searches of 256 MiB, twice:
-as one hc_search_batch call per m (the 100 searches overlap on library streams;
-`value`) and as 800 single hc_search calls (per_m single numbers, roofline).  L2 is
-flushed (2 x L2 bytes read) before every single search and every batch call,
-outside the timed intervals; the device time comes from CUDA events the library
-records on the caller's stream.  value = bytes searched / summed device time.
+of the config once with a single hc_search call (the north star's call: search
+kernel, count read-back, ordering of the positions into the caller's int64
+buffer), i.e. 800 searches of 256 MiB.  L2 is flushed (2 x L2 bytes read) before
+every call, outside the timed intervals; each call's device time comes from CUDA
+events the library records on the caller's stream (time_kernel = 2: from the
+search launch to the end of the call's last kernel, and the search kernel alone
+for the roofline).  value = bytes searched / summed device time.
+
+Reported beside it (never in `value`): the same patterns through hc_search_batch
+(one call per m; multi-pattern launches), per-m single-call numbers on C3 and C4,
+the end-to-end numbers through the host-buffer C-ABI calls, and the oracle on
+the host cores.
 
 Under torchrun (N>1), --mode replicas (default): every rank searches the same text
 with its own seeded patterns (weak scaling; no data-path collective, DESIGN.md 6);
@@ -25,7 +30,7 @@ time is its kernel time plus the exchange, value = n x searches / max over ranks
 
 --impl reference times the oracle (oracle/, plain C HC of Fig. 5 run over the
 host cores) on a bounded sample of the same workload: the base contract's
-reference arm for this tier (DESIGN.md 8).
+reference arm for this tier (DESIGN.md 10).
 """
 from __future__ import annotations
 
@@ -40,15 +45,16 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-PATH_NAMES = {1: "staged", 2: "gather", 3: "stream", 4: "shc"}
+PATH_NAMES = {1: "staged", 2: "gather", 3: "stream", 4: "shc", 5: "scan"}
 sys.path.insert(0, ROOT)
 
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
 METRIC = "text GB/s searched per pattern vs m (1 B200), % of HBM peak; bit-exact"
 # fraction of 32-B sectors HC touches, SURVEY.md 8(d) (simulated, DNA/protein/NL within 15%)
-F32 = {8: 1.0, 16: 1.0, 32: 1.0, 64: 0.63, 128: 0.29, 256: 0.145, 512: 0.075, 1024: 0.039,
-       2048: 0.019, 4096: 0.011, 2: 1.0, 4: 1.0}
+F32 = {2: 1.0, 4: 1.0, 8: 1.0, 16: 1.0, 32: 1.0, 64: 0.63, 128: 0.29, 256: 0.145, 512: 0.075,
+       1024: 0.039, 2048: 0.019, 4096: 0.011}
+TARGET_GBPS = 4000.0   # north star: >= 50% of the ~8 TB/s HBM peak for m >= 16
 
 
 def load_peaks():
@@ -124,6 +130,16 @@ def gen_workload(cfg, rank: int, per_m: int | None):
     return y, work
 
 
+def round_robin(work):
+    """Patterns in the order (m_0 #0, m_1 #0, ..., m_0 #1, ...): a bounded CPU sample then
+    covers every m."""
+    by_m = {}
+    for item in work:
+        by_m.setdefault(item[0], []).append(item)
+    return [lst[k] for k in range(max(len(v) for v in by_m.values())) for lst in by_m.values()
+            if k < len(lst)]
+
+
 def reference_arm(args, cfg, ws, rank):
     """Oracle (O2, Fig. 5 HC in plain C) over the host cores on a bounded sample."""
     if rank != 0:
@@ -131,18 +147,11 @@ def reference_arm(args, cfg, ws, rank):
     import oracle
     y, work = gen_workload(cfg, 0, args.per_m)
     T = os.cpu_count() or 1
-    budget = args.ref_seconds
-    by_m = {}
-    for item in work:
-        by_m.setdefault(item[0], []).append(item)
-    sample = [lst[k] for k in range(max(len(v) for v in by_m.values())) for lst in by_m.values()
-              if k < len(lst)]
-    # warm-up: one search
-    oracle.hc_threaded(sample[0][4], y, sample[0][1], sample[0][2], threads=T)
-    step_vals = []
+    sample = round_robin(work)
+    oracle.hc_threaded(sample[0][4], y, sample[0][1], sample[0][2], threads=T)   # warm-up
     done_total = 0
     t_total = 0.0
-    per_step = max(1, budget / max(1, args.steps))
+    per_step = max(1.0, args.ref_seconds / max(1, args.steps))
     idx = 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -155,7 +164,6 @@ def reference_arm(args, cfg, ws, rank):
             if time.perf_counter() - t0 > per_step:
                 break
         dt = time.perf_counter() - t0
-        step_vals.append(nb / dt / 1e9)
         done_total += nb
         t_total += dt
     v = done_total / t_total / 1e9
@@ -175,13 +183,12 @@ def reference_arm(args, cfg, ws, rank):
 
 
 def cpu_baseline(cfg, y, work, seconds: float):
+    """The oracle as it stands on the host cores: O2 threaded over window-end ranges on a
+    bounded sample (the reported baseline), and O2 on ONE thread per m (search only and
+    search + Preprocessing: the paper's own single-core measurement)."""
     import oracle
     T = os.cpu_count() or 1
-    by_m = {}
-    for item in work:
-        by_m.setdefault(item[0], []).append(item)
-    order = [lst[k] for k in range(max(len(v) for v in by_m.values())) for lst in by_m.values()
-             if k < len(lst)]
+    order = round_robin(work)
     t0 = time.perf_counter()
     nb = 0
     cnt = 0
@@ -191,9 +198,27 @@ def cpu_baseline(cfg, y, work, seconds: float):
         nb += len(y)
         cnt += 1
     dt = time.perf_counter() - t0
+    # single thread: one pattern per m on a 64 MiB slice of the text (bounded time)
+    ys = y[:min(len(y), 64 << 20)]
+    single = {}
+    seen = set()
+    for (m, q, a, o, x) in work:
+        if m in seen:
+            continue
+        seen.add(m)
+        t1 = time.perf_counter()
+        tab = oracle.preprocess(x, q, a)
+        t2 = time.perf_counter()
+        oracle.hc_search(x, ys, q, a, table=tab)
+        t3 = time.perf_counter()
+        single[str(m)] = {"GBps_search": round(len(ys) / (t3 - t2) / 1e9, 3),
+                          "GBps_incl_prepare": round(len(ys) / (t3 - t1) / 1e9, 3)}
     return {"value": round(nb / dt / 1e9, 3), "unit": "GB/s", "cores": T, "kind": "oracle",
             "sample": f"{cnt} searches of {len(y)} B (one pattern per m in turn, from the first), "
-                      f"O2 HC (oracle/hc_oracle.c) over {T} threads by window-end ranges"}
+                      f"O2 HC (oracle/hc_oracle.c) over {T} threads by window-end ranges",
+            "single_thread_per_m": single,
+            "single_thread_sample": f"O2 on one thread, first pattern of each m, first {len(ys)} B "
+                                    "of the text; incl_prepare adds Fig. 3 Preprocessing"}
 
 
 def main():
@@ -204,15 +229,16 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="hc", choices=["hc", "reference"])
     ap.add_argument("--per-m", type=int, default=None, help="patterns per m (default: config's)")
+    ap.add_argument("--extra-configs", default="C3,C4",
+                    help="configs whose per-m single-call numbers are added (not in value)")
+    ap.add_argument("--extra-per-m", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"])
-    ap.add_argument("--api", default="batch", choices=["batch", "single"],
-                    help="value from one hc_search_batch call per m (default) or from single "
-                         "hc_search calls; both are always measured and reported per m")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -267,107 +293,57 @@ def main():
     counts = [hc.search_raw(h, y.data_ptr(), n, None, 0, sp) for h in handles]
     cap = max(1, max(counts))
     pos = torch.empty(cap, dtype=torch.int64, device=dev)
-    opts = hc.Opts(path=0, time_kernel=1)
+    opts = hc.Opts(path=0, time_kernel=2)
     st = hc.Stats()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in work]
     if shard_mode:
-        from paper_2310_15711_b200.shard import shard_bounds
+        from paper_2310_15711_b200.shard import shard_bounds, gather_positions
         shards = {m: shard_bounds(n, m, ws, rank) for m in cfg.ms}
         xev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in work]
-        cnt_t = torch.zeros(1, dtype=torch.int64, device=dev)
-        pad = torch.full((cap,), -1, dtype=torch.int64, device=dev)
-        g_cnt = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
-        g_pos = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in range(ws)]
 
     def step(timed: bool):
+        """One step: every pattern through one hc_search call (the north star's call)."""
         per = []
         launches = 0
         for k, h in enumerate(handles):
             flush_l2()
-            e0, e1 = ev[k]
-            e0.record(stream)
             if shard_mode:
                 sh = shards[work[k][0]]
                 c = hc.search_raw(h, y.data_ptr() + sh.text_lo, sh.size, pos.data_ptr(), cap, sp,
                                   opts, st) if sh.size >= work[k][0] else 0
                 x0, x1 = xev[k]
                 x0.record(stream)
-                # exchange: counts, then the positions padded to cap
-                torch.add(pos[:c], sh.text_lo, out=pad[:c])   # global positions
-                if dist:
-                    cnt_t.fill_(c)
-                    dist.all_gather(g_cnt, cnt_t)
-                    dist.all_gather(g_pos, pad)
+                if dist:   # exchange sized to the actual counts (SURVEY 8(e))
+                    total, _ = gather_positions(pos[:c], sh.text_lo)
+                    if not timed:
+                        assert total == counts[k], (k, total, counts[k])
                 x1.record(stream)
             else:
                 c = hc.search_raw(h, y.data_ptr(), n, pos.data_ptr(), cap, sp, opts, st)
                 assert c == counts[k]
-            e1.record(stream)
             launches += st.launches
-            per.append((st.kernel_ms, st.path))
-            if shard_mode and not timed:
-                total = int(sum(t.item() for t in g_cnt)) if dist else c
-                assert total == counts[k], (k, total, counts[k])
+            per.append((st.kernel_ms, st.search_ms, st.path, st.reruns))
         torch.cuda.synchronize(dev)
-        calls = [e0.elapsed_time(e1) for (e0, e1) in ev]
-        # value uses the library's device time of each call's work (search launch to the
-        # end of its last kernel, CUDA events on the launching stream); the event pair
-        # around the Python call (host API overhead included) is reported as call time
-        times = [kms for (kms, _) in per]
+        times = [p[0] for p in per]
         if shard_mode:
             times = [t + x0.elapsed_time(x1) for t, (x0, x1) in zip(times, xev)]
-        return times, per, launches, calls
-
-    # hc_search_batch per m (all of its patterns in one call; replicas mode only)
-    use_batch = not shard_mode
-    by_m = {}
-    for k, (m, q, a, o, x) in enumerate(work):
-        by_m.setdefault(m, []).append(k)
-    if use_batch:
-        bufs = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in work]
-        bst = hc.Stats()
-
-    def batch_step(timed: bool):
-        tms = {}
-        nl = 0
-        for m, idx in by_m.items():
-            flush_l2()
-            got = hc.search_batch_raw([handles[k] for k in idx], y.data_ptr(), n,
-                                      [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp,
-                                      opts, bst)
-            assert got == [counts[k] for k in idx], m
-            tms[m] = bst.kernel_ms
-            nl += bst.launches          # search (single or multi-pattern) + finish kernels
-        return tms, nl
+        return times, per, launches
 
     for _ in range(args.warmup):
         step(False)
-        if use_batch:
-            batch_step(False)
 
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    all_times = []
-    all_kernel = []
-    all_calls = []
-    all_batch = []
+    all_times, all_per = [], []
     launches_total = 0
-    launches_batch = 0
     with Clocks(local) as clk:
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
-            times, per, launches, calls = step(True)
+            times, per, launches = step(True)
             all_times.append(times)
-            all_kernel.append(per)
-            all_calls.append(calls)
+            all_per.append(per)
             launches_total += launches
-            if use_batch:
-                bt, bl = batch_step(True)
-                all_batch.append(bt)
-                launches_batch += bl
         torch.cuda.synchronize(dev)
         t_wall = time.perf_counter() - t_wall0
     if dist:
@@ -375,11 +351,6 @@ def main():
     clocks = clk.summary()
 
     search_ms = sum(sum(t) for t in all_times)          # device time of all timed searches
-    value_api = "single"
-    if use_batch and args.api == "batch":
-        search_ms = sum(sum(bt.values()) for bt in all_batch)
-        value_api = "batch"
-        launches_total = launches_batch
     bytes_done = n * len(work) * args.steps
     if shard_mode:
         bytes_done /= ws                                 # each rank covers 1/ws of every search
@@ -395,61 +366,61 @@ def main():
     value = bytes_all / (search_ms_max / 1e3) / 1e9
 
     peak, peak_src = load_peaks()
-    # per-m breakdown (median over patterns and steps)
-    per_m = {}
+    by_m = {}
     for k, (m, q, a, o, x) in enumerate(work):
-        d = per_m.setdefault(m, {"t": [], "kt": [], "ct": [], "path": None, "q": q, "alpha": a,
-                                 "occ": 0})
-        for s in range(args.steps):
-            d["t"].append(all_times[s][k])
-            d["kt"].append(all_kernel[s][k][0])
-            d["ct"].append(all_calls[s][k])
-        d["path"] = PATH_NAMES[all_kernel[0][k][1]]
-        d["occ"] += counts[k]
-    per_m_out = {}
-    for m, d in per_m.items():
-        med = statistics.median(d["t"])
-        kmed = statistics.median(d["kt"])
-        per_m_out[str(m)] = {
-            "GBps_median": round(n / (med / 1e3) / 1e9, 1),
-            "GBps_min": round(n / (max(d["t"]) / 1e3) / 1e9, 1),
-            "GBps_max": round(n / (min(d["t"]) / 1e3) / 1e9, 1),
-            "device_us_median": round(med * 1e3, 2),
-            "call_us_median": round(statistics.median(d["ct"]) * 1e3, 2),
-            "call_GBps_median": round(n / (statistics.median(d["ct"]) / 1e3) / 1e9, 1),
-            "pct_of_measured_hbm": round(100 * n / (med / 1e3) / 1e9 / peak, 1),
-            "pct_of_8TBps": round(100 * n / (med / 1e3) / 1e9 / 8000, 1),
-            "q": d["q"], "alpha": d["alpha"], "path": d["path"],
-            "occ_per_pattern": round(d["occ"] / len(d["t"]) * args.steps, 2),
-            "prepare_us": round(prep_us[m][0], 2),
-            "prepare_batch_us_per_pattern": round(prep_us[m][1], 2),
-            "GBps_incl_prepare": round(n / ((med + prep_us[m][0] / 1e3) / 1e3) / 1e9, 1),
-        }
-        if use_batch:
-            bms = [bt[m] for bt in all_batch]
-            npat = len(by_m[m])
-            bmed = statistics.median(bms) / npat          # ms per pattern
-            per_m_out[str(m)]["batch_us_per_pattern"] = round(bmed * 1e3, 2)
-            per_m_out[str(m)]["batch_GBps"] = round(n / (bmed / 1e3) / 1e9, 1)
-            per_m_out[str(m)]["batch_pct_of_measured_hbm"] = round(100 * n / (bmed / 1e3) / 1e9 / peak, 1)
+        by_m.setdefault(m, []).append(k)
 
-    # roofline of the dominant kernel: the search kernel whose launches take the largest
-    # share of the step (the stream kernel on C2: m <= 32).  Algorithmic bytes per launch = f(m) * n +
+    def per_m_table(n_, work_, times_per_step, per_per_step, counts_, prep=None):
+        out = {}
+        bm = {}
+        for k, (m, q, a, o, x) in enumerate(work_):
+            bm.setdefault(m, []).append(k)
+        for m, ks in bm.items():
+            t = [times_per_step[s][k] for s in range(len(times_per_step)) for k in ks]
+            sk = [per_per_step[s][k][1] for s in range(len(per_per_step)) for k in ks]
+            med = statistics.median(t)
+            agg = n_ * len(t) / (sum(t) / 1e3) / 1e9
+            q, a = work_[ks[0]][1], work_[ks[0]][2]
+            d = {
+                "GBps_median": round(n_ / (med / 1e3) / 1e9, 1),
+                "GBps_aggregate": round(agg, 1),
+                "GBps_min": round(n_ / (max(t) / 1e3) / 1e9, 1),
+                "GBps_max": round(n_ / (min(t) / 1e3) / 1e9, 1),
+                "device_us_median": round(med * 1e3, 2),
+                "search_kernel_us_median": round(statistics.median(sk) * 1e3, 2),
+                "pct_of_measured_hbm": round(100 * n_ / (med / 1e3) / 1e9 / peak, 1),
+                "pct_of_8TBps": round(100 * n_ / (med / 1e3) / 1e9 / 8000, 1),
+                "meets_4000GBps": bool(n_ / (med / 1e3) / 1e9 >= TARGET_GBPS),
+                "q": q, "alpha": a, "path": PATH_NAMES.get(per_per_step[0][ks[0]][2], "?"),
+                "occ_per_pattern": round(sum(counts_[k] for k in ks) / len(ks), 2),
+                "patterns": len(ks),
+                "reruns": sum(per_per_step[s][k][3] for s in range(len(per_per_step)) for k in ks),
+            }
+            if prep is not None:
+                d["prepare_us"] = round(prep[m][0], 2)
+                d["prepare_batch_us_per_pattern"] = round(prep[m][1], 2)
+                d["GBps_incl_prepare"] = round(n_ / ((med + prep[m][0] / 1e3) / 1e3) / 1e9, 1)
+            out[str(m)] = d
+        return out
+
+    per_m_out = per_m_table(n, work, all_times, all_per, counts, prep_us)
+
+    # roofline of the dominant kernel: the search kernel (by path) whose launches take the
+    # largest share of `value`'s timed region.  Its duration per launch is the library's
+    # CUDA-event time around the search kernel alone (time_kernel = 2, same launches as
+    # `value`).  Algorithmic bytes per launch = f(m) * n (SURVEY 8(d) sector fractions) +
     # 4 B per position written.
-    shares = {}
-    for m, d in per_m.items():
-        shares[(d["path"])] = shares.get(d["path"], 0.0) + sum(d["kt"])
+    shares, alg, kt, nl = {}, {}, {}, {}
+    for s in range(args.steps):
+        for k, (m, q, a, o, x) in enumerate(work):
+            kms, sms, path, _ = all_per[s][k]
+            pn = PATH_NAMES.get(path, "?")
+            shares[pn] = shares.get(pn, 0.0) + sms
+            alg[pn] = alg.get(pn, 0.0) + F32.get(m, 1.0) * n + 4 * counts[k]
+            kt[pn] = kt.get(pn, 0.0) + sms / 1e3
+            nl[pn] = nl.get(pn, 0) + 1
     dom = max(shares, key=shares.get)
-    alg_bytes = 0.0
-    kt = 0.0
-    for k, (m, q, a, o, x) in enumerate(work):
-        path = PATH_NAMES[all_kernel[0][k][1]]
-        if path != dom:
-            continue
-        for s in range(args.steps):
-            alg_bytes += F32.get(m, 1.0) * n + 4 * counts[k]
-            kt += all_kernel[s][k][0] / 1e3
-    achieved = alg_bytes / kt / 1e9 if kt > 0 else 0.0
+    achieved = alg[dom] / kt[dom] / 1e9 if kt[dom] > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -457,8 +428,14 @@ def main():
     roofline = {"bound": "hbm", "kernel": f"{dom}_kernel (search)", "achieved": round(achieved, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "peak_source": peak_src,
-                "share_of_step": round(shares[dom] / sum(shares.values()), 3),
-                "algorithmic_bytes": "f(m) * n per launch (SURVEY 8(d) sector fractions) + 4 B/position"}
+                "launches": nl[dom], "avg_launch_us": round(1e6 * kt[dom] / nl[dom], 2),
+                "share_of_timed_region": round(shares[dom] / search_ms, 3),
+                "kernel_shares": {p_: round(v_ / search_ms, 3) for p_, v_ in shares.items()},
+                "other_kernels": {p_: {"achieved": round(alg[p_] / kt[p_] / 1e9, 1),
+                                       "frac": round(alg[p_] / kt[p_] / 1e9 / peak, 4)}
+                                  for p_ in shares if p_ != dom and kt[p_] > 0},
+                "algorithmic_bytes": "f(m) * n per launch (SURVEY 8(d) sector fractions; f = 1 "
+                                     "for m <= 32) + 4 B per position"}
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
@@ -470,98 +447,154 @@ def main():
                                        else f"{ws} replica(s), patterns split by rank"),
                        "patterns_per_m": len(work) // len(cfg.ms), "searches_per_step": len(work),
                        "qa": {str(m): list(cfg.qa[m]) for m in cfg.ms},
-                       "l2": "flushed (2 x L2 bytes read, clean eviction) before every single search and before every batch call, outside the timed intervals",
-                       "api": value_api,
-                       "timing": ("value: sum over m of the device time (CUDA events on the caller's "
-                                  "stream, recorded by the library) of one hc_search_batch call with "
-                                  "all of that m's patterns (the searches overlap on library streams; "
-                                  "each returns exactly its hc_search result); per_m also gives the "
-                                  "single hc_search calls (device time per call: search + finish "
-                                  "kernels) and the event time around each whole Python call")
-                                 if value_api == "batch" else
-                                 ("sum over searches of the library's CUDA-event device time per "
-                                  "hc_search call (search kernel with fused count publication, plus "
-                                  "the ordering kernels when they run); per_m also gives the event "
-                                  "time around the whole Python call (host API overhead included)"),
+                       "api": "hc_search (one call per pattern)",
+                       "l2": "flushed (2 x L2 bytes read, clean eviction) before every call, "
+                             "outside the timed intervals",
+                       "timing": "sum over calls of the library's CUDA-event device time per "
+                                 "hc_search call on the caller's stream (search kernel, finish "
+                                 "kernel, re-runs and large ordering when they run)",
                        "wall_ms_per_step_incl_flush": round(1000 * t_wall / args.steps, 2),
                        "text_sha256": I.sha256(y_np)[:16]},
             "pct_of_measured_hbm": round(100 * value / peak, 1),
             "pct_of_8TBps": round(100 * value / 8000, 1),
+            "target": {"GBps": TARGET_GBPS, "rule": ">= 4000 GB/s (50% of 8 TB/s) for every m >= 16",
+                       "m_meeting": [int(m) for m, d in per_m_out.items() if d["meets_4000GBps"]],
+                       "m_missing": [int(m) for m, d in per_m_out.items()
+                                     if int(m) >= 16 and not d["meets_4000GBps"]]},
             "per_m": per_m_out, "roofline": roofline, "clocks": clocks,
             "gpu_launches": launches_total}
 
+    # ------------------------------------------------------------ batch API (not value)
+    if not args.no_batch and not shard_mode:
+        bufs = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in work]
+        bst = hc.Stats()
+        bopts = hc.Opts(path=0, time_kernel=1)
+
+        def batch_step():
+            tms, nl_, rr = {}, 0, 0
+            for m, idx in by_m.items():
+                flush_l2()
+                got = hc.search_batch_raw([handles[k] for k in idx], y.data_ptr(), n,
+                                          [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp,
+                                          bopts, bst)
+                assert got == [counts[k] for k in idx], m
+                tms[m] = bst.kernel_ms
+                nl_ += bst.launches
+                rr += bst.reruns
+            return tms, nl_, rr
+
+        for _ in range(2):
+            batch_step()
+        bt_all, bl, brr = [], 0, 0
+        for _ in range(args.steps):
+            bt, l_, r_ = batch_step()
+            bt_all.append(bt)
+            bl += l_
+            brr += r_
+        bms = sum(sum(b.values()) for b in bt_all)
+        bper = {}
+        for m, idx in by_m.items():
+            tm = statistics.median([b[m] for b in bt_all]) / len(idx)
+            bper[str(m)] = {"us_per_pattern": round(tm * 1e3, 2),
+                            "GBps": round(n / (tm / 1e3) / 1e9, 1)}
+        line["batch"] = {"value": round(n * len(work) * args.steps / (bms / 1e3) / 1e9, 1),
+                         "unit": "GB/s", "api": "hc_search_batch, one call per m (up to 4 "
+                         "patterns per multi-pattern launch, 8 library streams)",
+                         "ms_per_step": round(bms / args.steps, 3), "gpu_launches": bl,
+                         "reruns": brr, "per_m": bper,
+                         "timing": "library CUDA events from the first launch to the end of the "
+                                   "call's re-runs, summed over m"}
+
+    # ------------------------------------------------------------ other configs (not value)
+    extra = [c for c in args.extra_configs.split(",") if c] if (ws == 1 and not shard_mode) else []
+    if extra:
+        line["configs"] = {}
+    for cname in extra:
+        ecfg = I.CONFIGS[cname]
+        ey_np, ework = gen_workload(ecfg, 0, args.extra_per_m)
+        ey = torch.from_numpy(ey_np).to(dev)
+        en = len(ey_np)
+        ehs = [hc.prepare(x, q, a) for (m, q, a, o, x) in ework]
+        ecnt = [hc.search_raw(h, ey.data_ptr(), en, None, 0, sp) for h in ehs]
+        epos = torch.empty(max(1, max(ecnt)), dtype=torch.int64, device=dev)
+        etimes, eper = [], []
+        for rep in range(3):
+            tt_, pp_ = [], []
+            for k, h in enumerate(ehs):
+                flush_l2()
+                c = hc.search_raw(h, ey.data_ptr(), en, epos.data_ptr(), epos.numel(), sp, opts, st)
+                assert c == ecnt[k]
+                tt_.append(st.kernel_ms)
+                pp_.append((st.kernel_ms, st.search_ms, st.path, st.reruns))
+            if rep > 0:                       # rep 0 is a warm-up
+                etimes.append(tt_)
+                eper.append(pp_)
+        tab = per_m_table(en, ework, etimes, eper, ecnt)
+        line["configs"][cname] = {
+            "workload": ecfg.name, "n": en, "patterns_per_m": args.extra_per_m,
+            "api": "hc_search", "calls_per_pattern": len(etimes), "per_m": tab,
+            "m_missing_4000GBps": [int(m) for m, d in tab.items() if int(m) >= 16 and not d["meets_4000GBps"]],
+            "text_sha256": I.sha256(ey_np)[:16]}
+        del ey, epos, ehs
+
     # ---------------------------------------------------------------- end to end
-    if not args.no_e2e:
+    if not args.no_e2e and not shard_mode:
+        # The whole step through the public host-buffer C-ABI: per step, hc_prepare_batch of
+        # every pattern (Fig. 3) and ONE hc_search_batch_host call with all of them
+        # (pinned host text in, H2D inside the call; positions D2H into pinned host
+        # buffers inside the call), wall clock.
         y_pin = torch.from_numpy(y_np).pin_memory()
-        ydev = torch.empty(n, dtype=torch.uint8, device=dev)
-        pos_pin = torch.empty(cap, dtype=torch.int64).pin_memory()
-        h2d = n + sum(len(x) for (_, _, _, _, x) in work)
-        d2h = 0
+        host_pos = [torch.empty(max(1, counts[k]), dtype=torch.int64).pin_memory() for k in range(len(work))]
         e2e_steps = max(1, min(args.steps, 2))
-        if shard_mode:
-            # this rank's text: the union of its slices over the m values
-            lo = min(sh.text_lo for sh in shards.values())
-            hi = max(sh.text_hi for sh in shards.values())
-            h2d = (hi - lo) + sum(len(x) for (_, _, _, _, x) in work)
+        qa_groups = {}
+        for k, (m, q, a, o, x) in enumerate(work):
+            qa_groups.setdefault((q, a), []).append(k)
         torch.cuda.synchronize(dev)
+
+        def e2e_step():
+            hs_all = [None] * len(work)
+            for (q, a), ks in qa_groups.items():
+                for k, h in zip(ks, hc.prepare_batch([work[k][4] for k in ks], q, a)):
+                    hs_all[k] = h
+            got = hc.search_batch_host_raw(hs_all, y_pin.data_ptr(), n,
+                                           [t.data_ptr() for t in host_pos],
+                                           [t.numel() for t in host_pos], sp)
+            for h in hs_all:
+                h.close()
+            return got
+
+        assert e2e_step() == counts
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            d2h = 0
-            if shard_mode:
-                ydev[lo:hi].copy_(y_pin[lo:hi], non_blocking=True)
-            else:
-                ydev.copy_(y_pin, non_blocking=True)
-            if use_batch and args.api == "batch":
-                for m, idx in by_m.items():
-                    t_m = time.perf_counter()
-                    hs = hc.prepare_batch([work[k][4] for k in idx], work[idx[0]][1],
-                                          work[idx[0]][2])
-                    got = hc.search_batch_raw(hs, ydev.data_ptr(), n,
-                                              [bufs[k].data_ptr() for k in idx], [cap] * len(idx), sp)
-                    for k, c in zip(idx, got):
-                        pos_pin[:c].copy_(bufs[k][:c], non_blocking=True)
-                        d2h += 8 + 8 * c
-                    for h in hs:
-                        h.close()
-                    torch.cuda.synchronize(dev)   # this m's positions are on the host
-                    if os.environ.get("HC_BENCH_DEBUG"):
-                        print(f"e2e m={m}: {1e3 * (time.perf_counter() - t_m):.2f} ms", file=sys.stderr)
-                continue
-            for (m, q, a, o, x), c in zip(work, counts):
-                h = hc.prepare(x, q, a)                       # host table + upload
-                if shard_mode:
-                    sh = shards[m]
-                    got = hc.search_raw(h, ydev.data_ptr() + sh.text_lo, sh.size, pos.data_ptr(),
-                                        cap, sp) if sh.size >= m else 0
-                    cnt_t.fill_(got)
-                    pad[:got] = pos[:got] + sh.text_lo
-                    if dist:
-                        dist.all_gather(g_cnt, cnt_t)
-                        dist.all_gather(g_pos, pad)
-                    if rank == 0:
-                        cs = [int(t.item()) for t in g_cnt] if dist else [got]
-                        parts = [g[:k] for g, k in zip(g_pos, cs)] if dist else [pad[:got]]
-                        res = torch.cat(parts)
-                        pos_pin[:res.numel()].copy_(res, non_blocking=True)
-                        d2h += 8 * len(cs) + 8 * res.numel()
-                else:
-                    got = hc.search_raw(h, ydev.data_ptr(), n, pos.data_ptr(), cap, sp)
-                    pos_pin[:got].copy_(pos[:got], non_blocking=True)
-                    d2h += 8 + 8 * got
-                h.close()
-            torch.cuda.synchronize(dev)
+            e2e_step()
         t_e2e = time.perf_counter() - t0
-        if dist:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
-        e2e_bytes = n * len(work) * e2e_steps * (1 if shard_mode else ws)
-        line["e2e"] = {"value": round(e2e_bytes / t_e2e / 1e9, 1), "unit": "GB/s",
+        h2d = n + sum(len(x) for (_, _, _, _, x) in work)
+        d2h = 8 * sum(counts)
+        # single-pattern end to end: hc_search_host (host text in, host positions out; the
+        # text crosses PCIe on every call), one pattern per m
+        single_t, single_n = 0.0, 0
+        seen = set()
+        for k, (m, q, a, o, x) in enumerate(work):
+            if m in seen:
+                continue
+            seen.add(m)
+            hp = host_pos[k]
+            t1 = time.perf_counter()
+            h = hc.prepare(x, q, a)
+            c = hc.lib().hc_search_host(h.ptr, y_pin.data_ptr(), n, hp.data_ptr(), hp.numel(), None)
+            single_t += time.perf_counter() - t1
+            single_n += n
+            assert c == counts[k]
+            h.close()
+        line["e2e"] = {"value": round(n * len(work) * e2e_steps / t_e2e / 1e9, 1), "unit": "GB/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "includes": "pinned H2D of the text, hc_prepare(_batch) of every pattern, "
-                                   + ("hc_search_batch per m" if (use_batch and args.api == "batch")
-                                      else "hc_search per pattern")
-                                   + ", D2H of counts and positions; wall clock"}
+                       "api": "hc_prepare_batch + one hc_search_batch_host call per step (host "
+                              "buffers in and out: the text H2D and every position D2H inside "
+                              "the call); wall clock",
+                       "single_call": {"value": round(single_n / single_t / 1e9, 2), "unit": "GB/s",
+                                       "api": "hc_prepare + hc_search_host per pattern (the "
+                                              "256 MiB text crosses PCIe on every call), one "
+                                              "pattern per m", "calls": len(seen)}}
 
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, y_np, work, args.cpu_seconds)

@@ -112,7 +112,9 @@ typedef struct hc_search_opts {
     int stages;       /* staged: TMA pipeline depth; stream: buffers per warp, 2..4 (0 = default 2) */
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
-    int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms) */
+    int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms);
+                         2: also around the search kernel alone (stats->search_ms; the extra
+                         event sits between the search and finish kernels) */
     int ctas_per_sm;  /* cap on resident CTAs per SM for the persistent grid (0 = occupancy max) */
     int debug;        /* must be 0.  Measurement-only modes (1 = copy pipeline alone, 3 = phase A
                          only, 5 = phase-B counters, 6 = filter on stale stage data; results NOT
@@ -137,9 +139,10 @@ typedef struct hc_search_stats {
     int64_t tiles;     /* staged: text tiles; gather: lane chunks */
     int launches;      /* kernels launched by this call (search, re-run, sort, copy) */
     int reruns;        /* search re-runs after the position scratch overflowed */
-    float kernel_ms;   /* if time_kernel: device time from the search launch to the end of the
-                          call's last kernel (search + result ordering), first attempt */
+    float kernel_ms;   /* if time_kernel: device time from the first search launch to the end
+                          of the call's last kernel (search, finish, re-runs, ordering) */
     uint32_t dbg[2];   /* instrumented build, debug == 5: phase-B loop iterations and calls */
+    float search_ms;   /* if time_kernel == 2: device time of the first search kernel alone */
 } hc_search_stats;
 
 /* hc_search with explicit options (NULL = defaults) and optional statistics (NULL = none). */
@@ -177,6 +180,16 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
  * hc_status. */
 int64_t hc_search_host(const hc_handle *h, const uint8_t *y_host, size_t n,
                        int64_t *pos_out_host, size_t max_out, cudaStream_t stream);
+
+/* End-to-end batch: hc_search_batch with HOST buffers.  Copies the n text bytes at y_host
+ * (pinned or pageable HOST memory) to a device buffer the call owns, runs
+ * hc_search_batch(hs, npat, ...) on it, and copies each pattern's min(count, max_out[i])
+ * positions back into pos_out_host[i] (HOST int64 buffers, or NULL entries / NULL array for
+ * counts only).  Synchronous; every copy and kernel is enqueued on `stream`.
+ * counts: HOST int64[npat].  Returns HC_OK or a negative hc_status. */
+int hc_search_batch_host(const hc_handle *const *hs, size_t npat, const uint8_t *y_host, size_t n,
+                         int64_t *counts, int64_t *const *pos_out_host, const size_t *max_out,
+                         cudaStream_t stream, const hc_search_opts *opts, hc_search_stats *stats);
 
 /* Frees the handle's host and device state.  No search on the handle may be in flight. */
 void hc_destroy(hc_handle *h);

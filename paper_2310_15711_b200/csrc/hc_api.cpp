@@ -143,6 +143,30 @@ void tune_pool(int dev) {
     });
 }
 
+// CUDA events of one timed call (time_kernel): ev0 .. ev1, and optionally a mid event.
+struct Events {
+    cudaEvent_t e0 = nullptr, em = nullptr, e1 = nullptr;
+    Events(bool on, bool mid) {
+        if (!on) return;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        if (mid) cudaEventCreate(&em);
+    }
+    ~Events() {
+        if (e0) cudaEventDestroy(e0);
+        if (em) cudaEventDestroy(em);
+        if (e1) cudaEventDestroy(e1);
+    }
+    void record0(cudaStream_t st) { if (e0) cudaEventRecord(e0, st); }
+    void record_mid(cudaStream_t st) { if (em) cudaEventRecord(em, st); }
+    void record1(cudaStream_t st) { if (e1) cudaEventRecord(e1, st); }
+    void elapsed(float *total, float *mid) {
+        if (!e1 || cudaEventSynchronize(e1) != cudaSuccess) return;
+        cudaEventElapsedTime(total, e0, e1);
+        if (em) cudaEventElapsedTime(mid, e0, em);
+    }
+};
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
@@ -602,8 +626,15 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
 
     int launches = 0, reruns = 0;
     uint32_t count = 0;
-    float kms = 0.f;
+    float kms = 0.f, sms = 0.f;
     hc::LaunchInfo li;
+    // time_kernel: ev0 before the first search launch, ev1 after the call's last kernel
+    // (re-runs and the large ordering included: the span then also holds the count
+    // read-back gaps); time_kernel = 2 also records evS right after the first search
+    // kernel, i.e. the search kernel alone (this event sits between the search and the
+    // PDL-launched finish kernel).
+    Events ev(o.time_kernel != 0, o.time_kernel >= 2);
+    ev.record0(stream);
     for (int attempt = 0;; ++attempt) {
         Scratch *sc = nullptr;
         cudaError_t e = get_scratch(h->device, cap, stream, &sc);
@@ -611,39 +642,26 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         p.counter = sc->buf;
         p.out = want_pos ? sc->buf + 4 : nullptr;
         p.cap = static_cast<uint32_t>(cap);
-        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-        const bool timed = o.time_kernel && attempt == 0;
-        if (timed) {
-            cudaEventCreate(&ev0);
-            cudaEventCreate(&ev1);
-            cudaEventRecord(ev0, stream);
-        }
         const char *stage = "search kernel launch";
         e = launch_search(path, p, stream, o, &li);
         ++launches;
-        if (timed && o.debug == 7) cudaEventRecord(ev1, stream);   // search kernel alone
+        if (attempt == 0) ev.record_mid(stream);
         if (e == cudaSuccess) {
             stage = "finish kernel launch";
             *sc->host_count = 0xffffffffu;
             // debug trace: the finish kernel's start / after-wait stamps follow the CTA stamps
             unsigned long long *ftr = nullptr;
-            if (o.trace) ftr = o.trace + static_cast<size_t>(li.grid) * p.trace_tiles * 4 + 2 * li.grid;
+            if (HC_INSTRUMENT && o.trace)
+                ftr = o.trace + static_cast<size_t>(li.grid) * p.trace_tiles * 4 + 2 * li.grid;
             e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, p.n, sc->host_count_dev, stream,
                                   ftr);
             ++launches;
         }
-        // device time of the call: search + finish (count publication, ordering of up to
-        // kSmallSort positions); a CUB ordering below extends it
-        if (timed && o.debug != 7) cudaEventRecord(ev1, stream);
         if (e == cudaSuccess) {
             stage = "search/finish execution";
             e = cudaStreamSynchronize(stream);
         }
         if (e != cudaSuccess) {
-            if (timed) {
-                cudaEventDestroy(ev0);
-                cudaEventDestroy(ev1);
-            }
             // the counter may be left non-zero: force a fresh scratch next time
             cudaFree(sc->buf);
             sc->buf = nullptr;
@@ -657,10 +675,6 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         }
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all
-            if (timed) {
-                cudaEventDestroy(ev0);
-                cudaEventDestroy(ev1);
-            }
             cap = count;
             ++reruns;
             continue;
@@ -668,17 +682,13 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         if (want_pos && count > hc::kSmallSort) {
             const uint32_t k = static_cast<uint32_t>(std::min<size_t>(count, max_out));
             e = hc::sort_large(sc->buf + 4, count, nn, pos_out, k, stream, &launches);
-            if (timed) cudaEventRecord(ev1, stream);   // includes the count read-back gap
             if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
             if (e != cudaSuccess) return cuda_fail(e, "sort");
         }
-        if (timed) {
-            if (cudaEventSynchronize(ev1) == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
-            cudaEventDestroy(ev0);
-            cudaEventDestroy(ev1);
-        }
         break;
     }
+    ev.record1(stream);
+    ev.elapsed(&kms, &sms);
     if (stats) {
         stats->path = path;
         stats->grid = li.grid;
@@ -688,6 +698,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         stats->launches = launches;
         stats->reruns = reruns;
         stats->kernel_ms = kms;
+        stats->search_ms = sms;
     }
     return static_cast<int64_t>(count);
 }
@@ -935,6 +946,55 @@ int64_t hc_search_host(const hc_handle *h, const uint8_t *y_host, size_t n, int6
     if (e != cudaSuccess) return cuda_fail(e, "hc_search_host read-back");
     if (e2 != cudaSuccess) return cuda_fail(e2, "hc_search_host sync");
     return cnt;
+}
+
+int hc_search_batch_host(const hc_handle *const *hs, size_t npat, const uint8_t *y_host, size_t n,
+                         int64_t *counts, int64_t *const *pos_out_host, const size_t *max_out,
+                         cudaStream_t stream, const hc_search_opts *opts, hc_search_stats *stats) {
+    if (npat == 0) return HC_OK;
+    if (!hs || !counts || (n > 0 && !y_host)) return fail(HC_EINVAL);
+    if (n > HC_MAX_TEXT) return fail(HC_ETOOLONG);
+    for (size_t i = 0; i < npat; ++i)
+        if (!hs[i]) return fail(HC_EINVAL);
+    g_last_error = HC_OK;
+    DeviceGuard guard(hs[0]->device);
+    tune_pool(hs[0]->device);
+    // one device block: the text, then each pattern's position buffer (8-byte aligned)
+    std::vector<size_t> off(npat + 1, 0);
+    const size_t ybytes = (n + 15) & ~size_t(15);
+    off[0] = ybytes;
+    for (size_t i = 0; i < npat; ++i) {
+        const bool want = pos_out_host && pos_out_host[i] && max_out && max_out[i] > 0 && n >= hs[i]->m;
+        const size_t k = want ? std::min<size_t>(max_out[i], n - hs[i]->m + 1) : 0;
+        off[i + 1] = off[i] + 8 * k;
+    }
+    uint8_t *blk = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&blk), std::max<size_t>(off[npat], 16), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "hc_search_batch_host alloc");
+    if (n > 0) e = cudaMemcpyAsync(blk, y_host, n, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(blk, stream);
+        return cuda_fail(e, "hc_search_batch_host upload");
+    }
+    std::vector<int64_t *> dpos(npat, nullptr);
+    std::vector<size_t> ks(npat, 0);
+    for (size_t i = 0; i < npat; ++i) {
+        ks[i] = (off[i + 1] - off[i]) / 8;
+        if (ks[i]) dpos[i] = reinterpret_cast<int64_t *>(blk + off[i]);
+    }
+    int rc = hc_search_batch(hs, npat, blk, n, counts, dpos.data(), ks.data(), stream, opts, stats);
+    if (rc == HC_OK) {
+        for (size_t i = 0; i < npat && e == cudaSuccess; ++i) {
+            const size_t k = std::min<size_t>(ks[i], counts[i] > 0 ? static_cast<size_t>(counts[i]) : 0);
+            if (k) e = cudaMemcpyAsync(pos_out_host[i], dpos[i], 8 * k, cudaMemcpyDeviceToHost, stream);
+        }
+    }
+    cudaFreeAsync(blk, stream);
+    const cudaError_t e2 = cudaStreamSynchronize(stream);
+    if (rc != HC_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "hc_search_batch_host read-back");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "hc_search_batch_host sync");
+    return HC_OK;
 }
 
 }  // extern "C"

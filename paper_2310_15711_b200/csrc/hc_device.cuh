@@ -194,7 +194,11 @@ struct FTable {
 };
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
 // top Q bytes are meaningful.  Reads just the aligned 8-byte words holding y[p]
-// and y[p-Q+1] (both inside the text), so no byte outside [0, n) is touched.
+// and y[p-Q+1] (both inside the text).  On global text such a word can extend up to
+// 7 bytes before y[0] or past y[n-1]: an aligned 8-byte word never crosses a page, so
+// this cannot fault, but a checker that tracks exact allocation sizes (compute-
+// sanitizer on a cudaMalloc of exactly n bytes) reports those bytes.  They never
+// influence a result (only the Q bytes of the q-gram are hashed).
 template <int Q, class T>
 __device__ __forceinline__ uint64_t end8(const T &t, uint32_t p) {
     auto a = t.addr(p);

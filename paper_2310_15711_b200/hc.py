@@ -33,7 +33,7 @@ WORD_BITS = 32
 
 # the symbols include/hc.h declares (tests check every one is exported)
 EXPORTS = ("hc_prepare", "hc_last_error", "hc_strerror", "hc_search", "hc_search_ex",
-           "hc_search_batch", "hc_prepare_batch", "hc_search_host", "hc_destroy", "hc_table", "hc_build_table",
+           "hc_search_batch", "hc_prepare_batch", "hc_search_host", "hc_search_batch_host", "hc_destroy", "hc_table", "hc_build_table",
            "hc_version")
 
 
@@ -48,7 +48,8 @@ class Opts(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("path", C.c_int), ("grid", C.c_int), ("block", C.c_int),
                 ("smem_bytes", C.c_int), ("tiles", C.c_int64), ("launches", C.c_int),
-                ("reruns", C.c_int), ("kernel_ms", C.c_float), ("dbg", C.c_uint32 * 2)]
+                ("reruns", C.c_int), ("kernel_ms", C.c_float), ("dbg", C.c_uint32 * 2),
+                ("search_ms", C.c_float)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
@@ -79,6 +80,11 @@ _lib.hc_prepare_batch.restype = C.c_int
 _lib.hc_search_host.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                                 C.c_void_p]
 _lib.hc_search_host.restype = C.c_int64
+_lib.hc_search_batch_host.argtypes = [C.POINTER(C.c_void_p), C.c_size_t, C.c_void_p, C.c_size_t,
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_size_t), C.c_void_p, C.POINTER(Opts),
+                                      C.POINTER(Stats)]
+_lib.hc_search_batch_host.restype = C.c_int
 _lib.hc_destroy.argtypes = [C.c_void_p]
 _lib.hc_destroy.restype = None
 _lib.hc_table.argtypes = [C.c_void_p, C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_int),
@@ -314,3 +320,35 @@ def search_host(h: Handle, y, max_out: int | None = None) -> np.ndarray:
         cap = cnt
         cnt, out = call(cap)
     return out[:min(cnt, cap)].copy()
+
+
+def search_batch_host_raw(handles, y_ptr: int, n: int, pos_ptrs, max_outs, stream_ptr: int = 0,
+                          opts: Opts | None = None, stats: Stats | None = None) -> list[int]:
+    """hc_search_batch_host on raw HOST pointers (text and per-pattern int64 buffers)."""
+    P = len(handles)
+    hs = (C.c_void_p * P)(*[h.ptr.value for h in handles])
+    counts = (C.c_int64 * P)()
+    pp = (C.c_void_p * P)(*pos_ptrs) if pos_ptrs is not None else None
+    mo = (C.c_size_t * P)(*max_outs) if max_outs is not None else None
+    rc = _lib.hc_search_batch_host(hs, P, C.c_void_p(y_ptr) if n else None, n, counts, pp, mo,
+                                   C.c_void_p(stream_ptr) if stream_ptr else None,
+                                   C.byref(opts) if opts is not None else None,
+                                   C.byref(stats) if stats is not None else None)
+    if rc != HC_OK:
+        raise HCError(int(rc), "hc_search_batch_host")
+    return list(counts)
+
+
+def search_batch_host(handles, y, max_out: int | None = None) -> list:
+    """hc_search_batch_host: y is host memory (numpy uint8); returns numpy int64 positions
+    per handle (exact when max_out is None: counts first, then the positions)."""
+    ya = _bytes(y)
+    n = len(ya)
+    yp = ya.ctypes.data if n else 0
+    if max_out is None:
+        mos = [max(c, 1) for c in search_batch_host_raw(handles, yp, n, None, None)]
+    else:
+        mos = [max(int(max_out), 1)] * len(handles)
+    outs = [np.empty(k, dtype=np.int64) for k in mos]
+    cnts = search_batch_host_raw(handles, yp, n, [o.ctypes.data for o in outs], mos)
+    return [o[:min(c, k)].copy() for o, c, k in zip(outs, cnts, mos)]

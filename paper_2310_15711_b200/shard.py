@@ -10,7 +10,9 @@ rank order; no merge is needed.
 
 There is one exchange step, over torch.distributed (NCCL on GPUs):
   1. all_gather of the per-rank counts (one int64 each);
-  2. all_gather of the position lists, padded to the largest count.
+  2. a variable-size all-gather of the position lists, sized to the actual counts
+     (all_to_all_single with output splits = the counts: rank r receives exactly
+     sum(counts) positions, no padding to the largest list).
 Both are negligible next to each rank reading its own n/world bytes.
 
 The per-rank search is `hc.search` (the CUDA path) unless a `searcher` is passed;
@@ -50,22 +52,28 @@ def shard_bounds(n: int, m: int, world: int, rank: int) -> Shard:
     return Shard(e_lo - m + 1, e_hi, e_lo, e_hi)
 
 
-def gather_positions(local: torch.Tensor, group=None) -> tuple[int, torch.Tensor]:
-    """All-gather of per-rank ascending int64 position lists (already global), in rank
-    order.  Returns (total count, concatenated positions) on every rank."""
+def gather_positions(local: torch.Tensor, offset: int = 0, group=None) -> tuple[int, torch.Tensor]:
+    """All-gather of per-rank ascending int64 position lists in rank order, each shifted by
+    its rank's `offset` (the slice's first text byte: positions become global).  The
+    exchange moves exactly the positions that exist (no padding).  Returns (total count,
+    concatenated positions) on every rank."""
     world = dist.get_world_size(group)
     dev = local.device
+    local = local.to(torch.int64)
+    if offset:
+        local = local + offset
     cnt = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
     counts = [int(c.item()) for c in counts]
-    width = max(max(counts), 1)
-    buf = torch.full((width,), -1, dtype=torch.int64, device=dev)
-    buf[:local.numel()] = local
-    outs = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(outs, buf, group=group)
-    pos = torch.cat([o[:c] for o, c in zip(outs, counts)])
-    return sum(counts), pos
+    total = sum(counts)
+    out = torch.empty(total, dtype=torch.int64, device=dev)
+    if total:
+        # variable all-gather: every rank sends its list to every rank
+        src = local.repeat(world) if local.numel() else local
+        dist.all_to_all_single(out, src, output_split_sizes=counts,
+                               input_split_sizes=[local.numel()] * world, group=group)
+    return total, out
 
 
 def _gpu_search(h, y_slice: torch.Tensor, max_out):
@@ -85,10 +93,10 @@ def search_sharded(h, y_slice: torch.Tensor, shard: Shard, max_out: int | None =
         raise ValueError("y_slice does not match the shard")
     search = searcher or _gpu_search
     if shard.size >= h.m:
-        local = search(h, y_slice, max_out).to(torch.int64) + shard.text_lo
+        local = search(h, y_slice, max_out).to(torch.int64)
     else:
         local = torch.empty(0, dtype=torch.int64, device=y_slice.device)
-    total, pos = gather_positions(local, group)
+    total, pos = gather_positions(local, shard.text_lo, group)
     if max_out is not None:
         pos = pos[:max_out]
     return total, pos

@@ -163,6 +163,36 @@ def test_host_entry_point():
     assert hc.search_host(h, y[:10]).tolist() == []
 
 
+def test_batch_host_entry_point():
+    """hc_search_batch_host: host text in, host positions out, every pattern equal to brute
+    force (mixed m, an absent pattern, max_out truncation, counts only)."""
+    rng = np.random.default_rng(58)
+    y = rng.integers(0, 4, 1_000_003, dtype=np.uint8)
+    pats = []
+    for m, q, a in [(8, 4, 12), (32, 6, 12), (300, 6, 12), (3, 2, 8)]:
+        o = int(rng.integers(0, len(y) - m))
+        pats.append((y[o:o + m].copy(), q, a))
+    pats.append((np.frombuffer(b"ACGTZ", np.uint8), 2, 10))
+    hs = [hc.prepare(x, q, a) for x, q, a in pats]
+    want = [oracle.brute(x, y) for x, _, _ in pats]
+    for g, w in zip(hc.search_batch_host(hs, y), want):
+        assert np.array_equal(g, w)
+    for g, w in zip(hc.search_batch_host(hs, y, max_out=3), want):
+        assert np.array_equal(g, w[:3])
+    assert hc.search_batch_host_raw(hs, y.ctypes.data, len(y), None, None) == [len(w) for w in want]
+
+
+def test_time_kernel_stats():
+    """time_kernel = 2: the search kernel's own device time is reported and lies inside
+    the call's device time."""
+    y = to_dev(I.gen_text("dna", 4_000_000, 59))
+    h = hc.prepare(y[1000:1032].cpu().numpy(), 6, 12)
+    _, st = hc.search(h, y, stats=True, time_kernel=2)
+    assert 0 < st["search_ms"] <= st["kernel_ms"]
+    _, st = hc.search(h, y, stats=True, time_kernel=1)
+    assert st["kernel_ms"] > 0 and st["search_ms"] == 0
+
+
 def test_errors():
     h = hc.prepare(b"abcd", 2, 8)
     with pytest.raises(hc.HCError) as ei:
