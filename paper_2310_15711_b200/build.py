@@ -51,15 +51,20 @@ def _compile(src: str, obj: str, defs: list, verbose: bool) -> None:
     subprocess.check_call(cmd)
 
 
-def build(force: bool = False, verbose: bool = False, instrument: bool = False) -> str:
-    """Compiles every translation unit (in parallel) and links the shared library."""
+def build(force: bool = False, verbose: bool = False, instrument: bool = False,
+          variant: str | None = None, defines: tuple = ()) -> str:
+    """Compiles every translation unit (in parallel) and links the shared library.
+    variant/defines: an experiment build libhc_<variant>.so with extra -D flags (A/B runs
+    in tools/, loaded through HC_LIB)."""
     lib = LIB_INSTR if instrument else LIB
+    if variant:
+        lib = os.path.join(HERE, f"libhc_{variant}.so")
     if not force and not _stale(lib):
         return lib
     from concurrent.futures import ThreadPoolExecutor
-    tag = "instr" if instrument else "prod"
+    tag = variant or ("instr" if instrument else "prod")
     os.makedirs(os.path.join(OBJ, tag), exist_ok=True)
-    defs = [f"-DHC_INSTRUMENT={1 if instrument else 0}"]
+    defs = [f"-DHC_INSTRUMENT={1 if instrument else 0}", *[f"-D{d}" for d in defines]]
     objs = [os.path.join(OBJ, tag, os.path.splitext(s)[0] + ".o") for s in SOURCES]
     with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
         list(ex.map(lambda so: _compile(so[0], so[1], defs, verbose), zip(SOURCES, objs)))
@@ -70,5 +75,7 @@ def build(force: bool = False, verbose: bool = False, instrument: bool = False) 
 
 
 if __name__ == "__main__":
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    defs = tuple(a.split("=", 1)[1] for a in sys.argv if a.startswith("--define="))
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
-                instrument="--instrument" in sys.argv))
+                instrument="--instrument" in sys.argv, variant=var, defines=defs))

@@ -34,7 +34,8 @@ struct hc_handle {
     std::vector<uint32_t> F;
     uint32_t m = 0, q = 0, alpha = 0, s = 0, mask = 0, hv = 0;
     int device = 0;
-    uint32_t *dF = nullptr;
+    uint32_t *dF = nullptr;        // device image: F | filter bitmap | x (zero-padded)
+    uint32_t *dFbits = nullptr;
     uint8_t *dx = nullptr;
     std::shared_ptr<void> block;   // hc_prepare_batch: device block shared by the batch
 };
@@ -85,8 +86,40 @@ void build_table(const uint8_t *x, uint32_t m, uint32_t q, uint32_t alpha, uint3
     *hv_out = h[m % q];                           // first q-gram of the chain ending at m-1
 }
 
-// Per-host-thread, per-device scratch: [counter (16 B) | positions (cap u32)] plus a
-// mapped pinned word the finish kernel writes the count into.  hc_search returns only
+// Device image of a handle's table, one allocation: F (2^alpha words) | the filter bitmap
+// (bit v set iff F[v] != 0: the l.6 test of Fig. 5 alone, 2^alpha bits, at least 16 B) |
+// x followed by at least 24 zero bytes.  Each part starts 16-byte aligned and has a
+// size that is a multiple of 16, so the kernels can move F and x with 1-D TMA bulk copies
+// and 16-byte loads without reading past the image.
+struct ImageLayout {
+    size_t f_off, bits_off, x_off, bytes;
+};
+ImageLayout image_layout(uint32_t alpha, size_t m) {
+    ImageLayout L;
+    const size_t fbytes = (size_t(1) << alpha) * sizeof(uint32_t);
+    L.f_off = 0;
+    L.bits_off = (fbytes + 15) & ~size_t(15);
+    L.x_off = L.bits_off + std::max<size_t>(16, ((size_t(1) << alpha) / 8 + 15) & ~size_t(15));
+    L.bytes = L.x_off + ((m + 24 + 15) & ~size_t(15));
+    return L;
+}
+void write_image(const hc_handle *h, uint8_t *dst) {   // dst: image_layout(...).bytes, zeroed
+    const ImageLayout L = image_layout(h->alpha, h->m);
+    std::memcpy(dst + L.f_off, h->F.data(), h->F.size() * sizeof(uint32_t));
+    uint32_t *bits = reinterpret_cast<uint32_t *>(dst + L.bits_off);
+    for (size_t v = 0; v < h->F.size(); ++v)
+        if (h->F[v]) bits[v >> 5] |= 1u << (v & 31);
+    std::memcpy(dst + L.x_off, h->x.data(), h->m);
+}
+void bind_image(hc_handle *h, uint8_t *base) {
+    const ImageLayout L = image_layout(h->alpha, h->m);
+    h->dF = reinterpret_cast<uint32_t *>(base + L.f_off);
+    h->dFbits = reinterpret_cast<uint32_t *>(base + L.bits_off);
+    h->dx = base + L.x_off;
+}
+
+// Per-host-thread, per-device scratch: [kCtr counter words | positions (cap u32)] plus
+// two mapped pinned words the search kernel's epilogue writes (count, ordered flag).  hc_search returns only
 // after all of its device work completed, so the next call on this thread (any
 // stream) can reuse it.  A new buffer's counter is zeroed by cudaMemsetAsync on the
 // stream that will use it (a plain cudaMemset runs on the legacy stream, which a
@@ -117,12 +150,13 @@ cudaError_t get_scratch(int dev, size_t cap, cudaStream_t st, Scratch **out) {
         if (sc.buf) cudaFree(sc.buf);
         sc.buf = nullptr;
         const size_t want = std::max<size_t>(cap, sc.cap + sc.cap / 2);
-        cudaError_t e = cudaMalloc(&sc.buf, 16 + want * sizeof(uint32_t));
+        // + 4 words: the epilogue copies positions in 16-byte pieces
+        cudaError_t e = cudaMalloc(&sc.buf, (hc::kCtr + want + 4) * sizeof(uint32_t));
         if (e != cudaSuccess) {
             sc.cap = 0;
             return e;
         }
-        e = cudaMemsetAsync(sc.buf, 0, 16, st);
+        e = cudaMemsetAsync(sc.buf, 0, hc::kCtr * sizeof(uint32_t), st);
         if (e != cudaSuccess) return e;
         sc.cap = want;
     }
@@ -204,7 +238,6 @@ constexpr uint32_t kDefaultStages = 2;
 // dynamic shared memory per staged CTA for 3 CTAs per SM: 228 KB per SM, 1 KB
 // reserved per CTA, 1.3 KB static
 constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
-constexpr uint32_t kDefaultSegPerLane = 2;
 constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per warp chunk
 constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
 constexpr uint32_t kDefaultStreamWarps = 8;     // stream path: warps per CTA
@@ -239,6 +272,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
     p.y = y_dev;
     p.n = nn;
     p.F = h->dF;
+    p.Fbits = h->dFbits;
     p.x = h->dx;
     p.m = m;
     p.q = q;
@@ -329,8 +363,16 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         p.block_warps = nw;
     }
     if (path == HC_PATH_GATHER) {
-        const uint32_t spl = o.seg_per_lane > 0 ? static_cast<uint32_t>(o.seg_per_lane)
-                                                : (S >= 512 ? 1u : kDefaultSegPerLane);
+        // lattice points per lane per chunk (1, 2 or 4; the chunk's loads go out together):
+        // 4 while every resident warp (about 32 per SM) still gets a chunk, fewer for the
+        // short lattices of large m, so that the latency-bound chains spread over all warps
+        uint32_t spl = 4;
+        if (o.seg_per_lane > 0) {
+            spl = o.seg_per_lane >= 4 ? 4u : (o.seg_per_lane >= 2 ? 2u : 1u);
+        } else {
+            const uint64_t warps = static_cast<uint64_t>(sm_count(h->device)) * 32u;
+            while (spl > 1 && K < warps * 32u * spl) spl /= 2;
+        }
         p.seg_per_chunk = 32 * spl;
         p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
         if (hc::gather_smem_bytes(p.alpha, m) > smem_budget(h->device)) return HC_EINVAL;
@@ -354,12 +396,12 @@ thread_local BatchRes g_batch[8];
 
 // Batch scratch of one pool stream: [kMaxPatterns counters of 16 B | positions], the
 // positions of a multi-pattern launch's pattern g at offset g * (cap / npat).
-constexpr size_t kCtrWords = 4 * hc::kMaxPatterns;
+constexpr size_t kCtrWords = hc::kCtr * hc::kMaxPatterns;
 cudaError_t batch_scratch(Scratch &sc, size_t cap, cudaStream_t st) {
     if (!sc.buf || sc.cap < cap) {
         if (sc.buf) cudaFree(sc.buf);
         sc.buf = nullptr;
-        cudaError_t e = cudaMalloc(&sc.buf, (kCtrWords + cap) * sizeof(uint32_t));
+        cudaError_t e = cudaMalloc(&sc.buf, (kCtrWords + cap + 4) * sizeof(uint32_t));
         if (e != cudaSuccess) {
             sc.cap = 0;
             return e;
@@ -390,7 +432,7 @@ cudaError_t batch_res(int dev, size_t npat, BatchRes **out) {
         r.ncounts = 0;
         void *hp = nullptr;
         const size_t want = std::max<size_t>(npat, 256);
-        cudaError_t e = cudaHostAlloc(&hp, want * 4, cudaHostAllocMapped | cudaHostAllocPortable);
+        cudaError_t e = cudaHostAlloc(&hp, want * 8, cudaHostAllocMapped | cudaHostAllocPortable);
         if (e != cudaSuccess) return e;
         void *dp = nullptr;
         e = cudaHostGetDevicePointer(&dp, hp, 0);
@@ -464,11 +506,17 @@ hc_handle *hc_prepare(const uint8_t *x, size_t m, int q, int alpha) {
         g_last_error = HC_ENODEV;
         return nullptr;
     }
-    e = cudaMalloc(&h->dF, h->F.size() * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&h->dx, m + 16);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(h->dF, h->F.data(), h->F.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(h->dx, x, m, cudaMemcpyHostToDevice);
+    {
+        const ImageLayout L = image_layout(h->alpha, h->m);
+        std::vector<uint8_t> img(L.bytes, 0);
+        write_image(h, img.data());
+        void *base = nullptr;
+        e = cudaMalloc(&base, L.bytes);
+        if (e == cudaSuccess) {
+            bind_image(h, static_cast<uint8_t *>(base));
+            e = cudaMemcpy(base, img.data(), L.bytes, cudaMemcpyHostToDevice);
+        }
+    }
     if (e != cudaSuccess) {
         cuda_fail(e, "hc_prepare upload");
         hc_destroy(h);
@@ -523,10 +571,9 @@ int hc_prepare_batch(const uint8_t *const *xs, const size_t *ms, size_t P, int q
         cuda_fail(e, "cudaGetDevice");
         return fail(HC_ENODEV);
     }
-    // host tables (Fig. 3 per pattern), laid out as the device block: F | x per pattern
-    const size_t fbytes = (size_t(1) << alpha) * sizeof(uint32_t);
+    // host tables (Fig. 3 per pattern), laid out as the device block: one image per pattern
     std::vector<size_t> off(P + 1, 0);
-    for (size_t i = 0; i < P; ++i) off[i + 1] = off[i] + ((fbytes + 15) & ~size_t(15)) + ((ms[i] + 16 + 15) & ~size_t(15));
+    for (size_t i = 0; i < P; ++i) off[i + 1] = off[i] + image_layout(static_cast<uint32_t>(alpha), ms[i]).bytes;
     std::vector<hc_handle *> hs(P, nullptr);
     std::vector<uint8_t> staging(off[P], 0);
     for (size_t i = 0; i < P; ++i) {
@@ -544,8 +591,7 @@ int hc_prepare_batch(const uint8_t *const *xs, const size_t *ms, size_t P, int q
         h->x.assign(xs[i], xs[i] + ms[i]);
         h->F.assign(size_t(1) << alpha, 0u);
         build_table(xs[i], h->m, h->q, h->alpha, h->F.data(), &h->s, &h->hv);
-        std::memcpy(staging.data() + off[i], h->F.data(), fbytes);
-        std::memcpy(staging.data() + off[i] + ((fbytes + 15) & ~size_t(15)), xs[i], ms[i]);
+        write_image(h, staging.data() + off[i]);
     }
     size_t cls = 0;
     void *blk = block_get(dev, off[P], &cls);
@@ -560,9 +606,7 @@ int hc_prepare_batch(const uint8_t *const *xs, const size_t *ms, size_t P, int q
     // in flight, as for hc_prepare handles)
     std::shared_ptr<void> block(blk, [dev, cls](void *p) { block_put(dev, cls, p); });
     for (size_t i = 0; i < P; ++i) {
-        uint8_t *base = static_cast<uint8_t *>(blk) + off[i];
-        hs[i]->dF = reinterpret_cast<uint32_t *>(base);
-        hs[i]->dx = base + ((fbytes + 15) & ~size_t(15));
+        bind_image(hs[i], static_cast<uint8_t *>(blk) + off[i]);
         hs[i]->block = block;
         hs_out[i] = hs[i];
     }
@@ -572,9 +616,8 @@ int hc_prepare_batch(const uint8_t *const *xs, const size_t *ms, size_t P, int q
 
 void hc_destroy(hc_handle *h) {
     if (!h) return;
-    if (!h->block) {   // hc_prepare: own allocations (batch handles share h->block)
+    if (!h->block) {   // hc_prepare: own allocation (batch handles share h->block)
         if (h->dF) cudaFree(h->dF);
-        if (h->dx) cudaFree(h->dx);
     }
     delete h;
 }
@@ -629,10 +672,9 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
     float kms = 0.f, sms = 0.f;
     hc::LaunchInfo li;
     // time_kernel: ev0 before the first search launch, ev1 after the call's last kernel
-    // (re-runs and the large ordering included: the span then also holds the count
-    // read-back gaps); time_kernel = 2 also records evS right after the first search
-    // kernel, i.e. the search kernel alone (this event sits between the search and the
-    // PDL-launched finish kernel).
+    // (re-recorded after a re-run or a host-launched ordering: the span then also holds
+    // the count read-back gaps); time_kernel = 2 also keeps evS right after the first
+    // search kernel (search + fused epilogue, one kernel).
     Events ev(o.time_kernel != 0, o.time_kernel >= 2);
     ev.record0(stream);
     for (int attempt = 0;; ++attempt) {
@@ -640,38 +682,33 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         cudaError_t e = get_scratch(h->device, cap, stream, &sc);
         if (e != cudaSuccess) return cuda_fail(e, "scratch");
         p.counter = sc->buf;
-        p.out = want_pos ? sc->buf + 4 : nullptr;
+        p.out = want_pos ? sc->buf + hc::kCtr : nullptr;
         p.cap = static_cast<uint32_t>(cap);
-        const char *stage = "search kernel launch";
+        p.host_count = sc->host_count_dev;
+        p.dst = want_pos ? pos_out : nullptr;
+        p.k_out = k_out;
+        p.nbits = hc::bits_for(nn);
+        sc->host_count[0] = 0xffffffffu;
+        sc->host_count[1] = 0;
+        // one kernel: search + fused epilogue (count publication, ordering when it can)
         e = launch_search(path, p, stream, o, &li);
         ++launches;
         if (attempt == 0) ev.record_mid(stream);
-        if (e == cudaSuccess) {
-            stage = "finish kernel launch";
-            *sc->host_count = 0xffffffffu;
-            // debug trace: the finish kernel's start / after-wait stamps follow the CTA stamps
-            unsigned long long *ftr = nullptr;
-            if (HC_INSTRUMENT && o.trace)
-                ftr = o.trace + static_cast<size_t>(li.grid) * p.trace_tiles * 4 + 2 * li.grid;
-            e = hc::launch_finish(sc->buf, p.out, p.cap, pos_out, k_out, p.n, sc->host_count_dev, stream,
-                                  ftr);
-            ++launches;
-        }
-        if (e == cudaSuccess) {
-            stage = "search/finish execution";
-            e = cudaStreamSynchronize(stream);
-        }
+        ev.record1(stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
         if (e != cudaSuccess) {
-            // the counter may be left non-zero: force a fresh scratch next time
+            // the counters may be left non-zero: force a fresh scratch next time
             cudaFree(sc->buf);
             sc->buf = nullptr;
             sc->cap = 0;
-            return cuda_fail(e, stage);
+            return cuda_fail(e, "search kernel");
         }
-        count = *reinterpret_cast<volatile uint32_t *>(sc->host_count);
+        const volatile uint32_t *hcnt = sc->host_count;
+        count = hcnt[0];
+        const bool ordered = hcnt[1] != 0;
         if (HC_INSTRUMENT && o.debug == 5 && stats) {
-            cudaMemcpy(stats->dbg, sc->buf + 2, 8, cudaMemcpyDeviceToHost);
-            cudaMemset(sc->buf + 2, 0, 8);
+            cudaMemcpy(stats->dbg, sc->buf + 4, 8, cudaMemcpyDeviceToHost);
+            cudaMemset(sc->buf + 4, 0, 8);
         }
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all
@@ -679,15 +716,17 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             ++reruns;
             continue;
         }
-        if (want_pos && count > hc::kSmallSort) {
+        if (want_pos && count > 0 && !ordered) {
+            // more positions than the epilogue's shared memory holds (or clustered): order
+            // them on the device from the scratch (hc_finish.cu)
             const uint32_t k = static_cast<uint32_t>(std::min<size_t>(count, max_out));
-            e = hc::sort_large(sc->buf + 4, count, nn, pos_out, k, stream, &launches);
+            e = hc::order_positions(sc->buf + hc::kCtr, count, nn, pos_out, k, stream, &launches);
+            ev.record1(stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-            if (e != cudaSuccess) return cuda_fail(e, "sort");
+            if (e != cudaSuccess) return cuda_fail(e, "ordering");
         }
         break;
     }
-    ev.record1(stream);
     ev.elapsed(&kms, &sms);
     if (stats) {
         stats->path = path;
@@ -767,9 +806,11 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
     };
     for (size_t i = 0; i < npat;) {
         const hc_handle *h = hs[i];
-        r->hcounts[i] = 0xffffffffu;
+        r->hcounts[2 * i] = 0xffffffffu;
+        r->hcounts[2 * i + 1] = 0;
         if (n < h->m) {
-            r->hcounts[i] = 0;
+            r->hcounts[2 * i] = 0;
+            r->hcounts[2 * i + 1] = 1;
             ++i;
             continue;
         }
@@ -827,9 +868,11 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
             if (pos_out && pos_out[i + t] && mo > 0)
                 cap = std::max(cap, std::min<size_t>(std::max<size_t>(mo, size_t(1) << 16), windows));
         }
-        e = batch_scratch(sc, std::max<size_t>(cap * g, 1), r->st[j]);
+        const size_t stride = (cap + 3) & ~size_t(3);   // 16-byte aligned per-pattern regions
+        e = batch_scratch(sc, std::max<size_t>(stride * g, 1), r->st[j]);
         if (e != cudaSuccess) return bail(cuda_fail(e, "batch scratch"));
         hc::LaunchInfo li;
+        p.nbits = hc::bits_for(nn);
         if (g == 1) {
             const size_t mo = max_out ? max_out[i] : 0;
             const bool want_pos = pos_out && pos_out[i] && mo > 0;
@@ -837,6 +880,10 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
             p.counter = sc.buf;
             p.out = want_pos ? sc.buf + kCtrWords : nullptr;
             p.cap = static_cast<uint32_t>(caps[i]);
+            p.host_count = r->hcounts_dev + 2 * i;
+            p.dst = want_pos ? pos_out[i] : nullptr;
+            p.k_out = want_pos ? static_cast<uint32_t>(std::min<size_t>(mo, windows)) : 0u;
+            r->hcounts[2 * i + 1] = 0;
             e = launch_search(path, p, r->st[j], o, &li);
         } else {
             hc::MParams mp{};
@@ -849,40 +896,36 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
                 mp.F[t] = ht->dF;
                 mp.x[t] = ht->dx;
                 mp.hv[t] = ht->hv;
-                mp.counter[t] = sc.buf + 4 * t;
-                mp.out[t] = want_pos ? sc.buf + kCtrWords + t * cap : nullptr;
+                mp.counter[t] = sc.buf + hc::kCtr * t;
+                mp.out[t] = want_pos ? sc.buf + kCtrWords + t * stride : nullptr;
                 mp.cap[t] = static_cast<uint32_t>(caps[i + t]);
+                mp.host_count[t] = r->hcounts_dev + 2 * (i + t);
+                mp.dst[t] = want_pos ? pos_out[i + t] : nullptr;
+                mp.k_out[t] = want_pos ? static_cast<uint32_t>(std::min<size_t>(mo, windows)) : 0u;
+                r->hcounts[2 * (i + t)] = 0xffffffffu;
+                r->hcounts[2 * (i + t) + 1] = 0;
             }
             e = hc::launch_mstream(p, mp, r->st[j], o.max_ctas, o.ctas_per_sm, &li);
         }
         ++launches;
-        for (size_t t = 0; t < g && e == cudaSuccess; ++t) {
-            const size_t mo = max_out ? max_out[i + t] : 0;
-            const bool want_pos = pos_out && pos_out[i + t] && mo > 0;
-            uint32_t *ctr = sc.buf + 4 * t;
-            const uint32_t *pos = want_pos ? sc.buf + kCtrWords + t * cap : nullptr;
-            e = hc::launch_finish(ctr, pos, static_cast<uint32_t>(caps[i + t]),
-                                  want_pos ? pos_out[i + t] : nullptr,
-                                  want_pos ? static_cast<uint32_t>(std::min<size_t>(mo, windows)) : 0u,
-                                  p.n, r->hcounts_dev + i + t, r->st[j]);
-            ++launches;
-        }
         if (e != cudaSuccess) return bail(cuda_fail(e, "batch launch"));
         i += g;
     }
     join_pool();
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return bail(cuda_fail(e, "batch execution"));
-    // patterns whose positions did not fit the scratch or need the large ordering are run
-    // again on their own (their counts are exact already); the device time of the batch
+    // patterns whose positions did not fit the scratch, or that the epilogue could not
+    // order (the pool scratch has been reused since), are run again on their own (their
+    // counts are exact already); the device time of the batch
     // (stats->kernel_ms) runs to the end of these re-runs
     int reruns = 0;
     for (size_t i = 0; i < npat; ++i) {
-        const uint32_t c = reinterpret_cast<volatile uint32_t *>(r->hcounts)[i];
+        const uint32_t c = reinterpret_cast<volatile uint32_t *>(r->hcounts)[2 * i];
+        const bool ordered = reinterpret_cast<volatile uint32_t *>(r->hcounts)[2 * i + 1] != 0;
         counts[i] = c;
         const size_t mo = max_out ? max_out[i] : 0;
         const bool want_pos = pos_out && pos_out[i] && mo > 0;
-        if (want_pos && c > 0 && (c > caps[i] || c > hc::kSmallSort)) {
+        if (want_pos && c > 0 && (c > caps[i] || !ordered)) {
             hc_search_opts orr = o;
             orr.time_kernel = 0;
             hc_search_stats rs{};

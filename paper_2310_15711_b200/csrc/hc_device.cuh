@@ -36,6 +36,10 @@
 #ifndef HC_INSTRUMENT
 #define HC_INSTRUMENT 0
 #endif
+#ifndef HC_LDG_MODE
+#define HC_LDG_MODE 1   // global text words: 0 = ld.global.nc, 1 = + .L2::64B (default: measured
+                        // 293 -> 167 MB DRAM read at C2 m = 128), 2 = + L1::no_allocate
+#endif
 
 namespace hc {
 
@@ -60,6 +64,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_inval(uint64_t *bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -141,7 +148,17 @@ struct GlobalText {
         return reinterpret_cast<uintptr_t>(y) + p;
     }
     __device__ __forceinline__ uint64_t word(uintptr_t aligned) const {
+#if HC_LDG_MODE == 1
+        uint64_t r;
+        asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(r) : "l"(aligned));
+        return r;
+#elif HC_LDG_MODE == 2
+        uint64_t r;
+        asm("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(r) : "l"(aligned));
+        return r;
+#else
         return __ldg(reinterpret_cast<const unsigned long long *>(aligned));
+#endif
     }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return __ldg(y + p); }
     __device__ __forceinline__ GlobalText shfl(uint32_t) const { return *this; }  // same in all lanes
@@ -192,6 +209,16 @@ struct FTable {
     __device__ __forceinline__ uint32_t operator[](uint32_t v) const { return lds32(base + 4 * v); }
     __device__ __forceinline__ bool pass(uint32_t v) const { return (*this)[v] != 0u; }   // l.6
 };
+// The filter bitmap (2^alpha bits, bit v set iff F[v] != 0) in shared memory: the l.6
+// test alone, 32x smaller than F, so it loads in one short round trip while F itself
+// arrives by a TMA bulk copy behind it.
+struct FBits {
+    uint32_t base;
+    __device__ __forceinline__ bool pass(uint32_t v) const {
+        return (lds32(base + 4 * (v >> 5)) >> (v & 31)) & 1u;
+    }
+};
+
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
 // top Q bytes are meaningful.  Reads just the aligned 8-byte words holding y[p]
 // and y[p-Q+1] (both inside the text).  On global text such a word can extend up to
@@ -416,9 +443,9 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
     uint32_t e = 0, i = 0, z = 0, v = 0, wsteps = 0;
     bool walk = false;
     const bool long_walks = p.m >= 2 * kLongWalk * Q;   // warp-wide walks can pay off
-    if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 3, 1u);
+    if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 5, 1u);
     while (__any_sync(HC_FULL, active)) {
-        if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 2, 1u);
+        if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 4, 1u);
         bool need_v = false, stepped = false;
         if (long_walks) {
             // walks that passed kLongWalk link tests and still have >= kLongWalk steps to
@@ -582,13 +609,16 @@ __device__ __forceinline__ void filter_lattice(const KParams &p, const T &txt, c
 
 // first_steps: the first steps of Fig. 5 for the window e = a_k of a lattice survivor
 // (F[v_0] != 0 already, l.6), evaluated lane-parallel, when m >= 2q: the walk's first
-// step (l.9-12) tests the link bit of v_1 = h(y[e-2q+1..e-q]) in F[v_0]; if it is
-// clear the loop breaks and the next window ends at j = e - q + S (l.18); if
-// F[h(j)] == 0 that window shifts by S again (l.6) to j + S >= a_k + S, out of
-// the segment (R11), and the segment is finished (returns false).  Otherwise the
-// segment continues at `start` = e (link set) or j.  Exact: these are the paper's
-// steps in order, with the three hashes loaded in parallel.  On DNA this finishes
-// ~90% of the lattice survivors for one memory round trip per 32.
+// step (l.9-12) tests the link bit of v_1 = h(y[e-2q+1..e-q]) in F[v_0]; if it is clear
+// the loop breaks and the next window ends at j = e - q + S (l.18).  If F[h(j)] == 0
+// that window shifts by S again (l.6) to j + S >= a_k + S, out of the segment
+// (R11), and the segment is finished.  Otherwise window j takes its own first walk step
+// (l.7-12): if the link bit of h(j - q) is clear in F[h(j)] the loop breaks again and
+// the next window ends at j - q + S = a_k - 2q + 2S, which is past the segment when
+// S >= 2q: finished as well.  Otherwise the segment continues at `start` = e (first
+// link set) or j.  Exact: these are the paper's steps in order, with the four hashes
+// loaded in parallel (one memory round trip).  On DNA this finishes ~95% of the lattice
+// survivors.
 template <int Q, int SH, class T, class FT>
 __device__ __forceinline__ bool first_steps_eval(const KParams &p, const T &txt, const FT &sF,
                                                  bool act, uint32_t e, uint32_t &start) {
@@ -598,13 +628,29 @@ __device__ __forceinline__ bool first_steps_eval(const KParams &p, const T &txt,
     const uint32_t j = e - Q + p.S;
     const bool jin = j < p.n;                            // else the break leaves the text
     const uint64_t W0 = end8<Q>(txt, e), W1 = end8<Q>(txt, e - Q);
-    const uint64_t W2 = end8<Q>(txt, jin ? j : e);
+    const uint64_t W2 = end8<Q>(txt, jin ? j : e), W3 = end8<Q>(txt, jin ? j - Q : e);
     const uint32_t v1 = qhash<Q, SH>(W1, p.mask);
+    const uint32_t v3 = qhash<Q, SH>(W3, p.mask);
     const uint32_t z0 = sF[qhash<Q, SH>(W0, p.mask)];
     const uint32_t z2 = sF[qhash<Q, SH>(W2, p.mask)];
-    if (((z0 >> (v1 & (kWordBits - 1))) & 1u) != 0u) return true;   // link set: walk on
+    if (((z0 >> (v1 & (kWordBits - 1))) & 1u) != 0u) {  // link set: walk on
+        if constexpr (!T::kLoSafe) {
+            // the walk will read back through the window (a true occurrence walks all of
+            // it, then verifies it): start its lines on their way to L2 now, so that the
+            // phase-B round trips of this segment hit L2 instead of DRAM
+            if (p.m >= 64) {
+                const uintptr_t lo = txt.addr(e + 1 - p.m) & ~static_cast<uintptr_t>(127);
+                for (uintptr_t a = lo; a <= txt.addr(e); a += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+            }
+        }
+        return true;
+    }
     start = j;                                           // break at the first step
-    return jin && z2 != 0u;
+    if (!jin || z2 == 0u) return false;                  // window j shifts out (l.6, l.18)
+    if (p.S >= 2 * Q && ((z2 >> (v3 & (kWordBits - 1))) & 1u) == 0u)
+        return false;                                    // window j breaks at its first step
+    return true;
 }
 
 // Gather path sink: lattice survivors (k) are queued per warp (q1) and run 32 at a
@@ -679,17 +725,45 @@ struct WarpQueueSink {
 __host__ __device__ inline uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
 __device__ __forceinline__ void load_table(const KParams &p, uint32_t *sF, uint8_t *sx) {
+    // F (2^alpha words) and x, with every thread's loads issued before its stores: one
+    // L2 round trip for the whole table instead of one per loop trip
     const uint32_t nF = 1u << p.alpha;
     if (nF >= 4) {
         const uint4 *src = reinterpret_cast<const uint4 *>(p.F);
         uint4 *dst = reinterpret_cast<uint4 *>(sF);
-        for (uint32_t w = threadIdx.x; w < nF / 4; w += blockDim.x) dst[w] = __ldg(src + w);
+        const uint32_t n4 = nF / 4;
+        for (uint32_t w0 = threadIdx.x; w0 < n4; w0 += 8 * blockDim.x) {
+            uint4 v[8];
+#pragma unroll
+            for (uint32_t r = 0; r < 8; ++r) {
+                const uint32_t w = w0 + r * blockDim.x;
+                if (w < n4) v[r] = __ldg(src + w);
+            }
+#pragma unroll
+            for (uint32_t r = 0; r < 8; ++r) {
+                const uint32_t w = w0 + r * blockDim.x;
+                if (w < n4) dst[w] = v[r];
+            }
+        }
     } else {
         for (uint32_t w = threadIdx.x; w < nF; w += blockDim.x) sF[w] = __ldg(p.F + w);
     }
-    for (uint32_t k = threadIdx.x; k < p.m; k += blockDim.x) sx[k] = __ldg(p.x + k);
-    // zero the 8-byte tail so 8-byte compares of x never read uninitialised bytes
-    if (threadIdx.x < 8) sx[p.m + threadIdx.x] = 0;
+    // x in 16-byte vectors (the device copy of x has >= 15 readable bytes past m), with
+    // the bytes from m on zeroed up to m + 8 so that 8-byte compares of x never read
+    // uninitialised shared memory
+    const uint32_t n16 = (p.m + 8 + 15) / 16;
+    for (uint32_t w = threadIdx.x; w < n16; w += blockDim.x) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (16 * w < p.m) v = __ldg(reinterpret_cast<const uint4 *>(p.x) + w);
+        uint32_t *vw = reinterpret_cast<uint32_t *>(&v);
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t b = 16 * w + 4 * j;
+            if (b >= p.m) vw[j] = 0;
+            else if (b + 4 > p.m) vw[j] &= (1u << (8 * (p.m - b))) - 1u;
+        }
+        reinterpret_cast<uint4 *>(sx)[w] = v;
+    }
 }
 
 __device__ __forceinline__ uint32_t ld_volatile_shared(const uint32_t *a) {
@@ -742,7 +816,8 @@ __device__ __forceinline__ StreamChunk stream_chunk(const KParams &p, uint32_t c
         return g;
     }
     // bytes [a_k0 - 2q + 1, a_{k1} - q]: the lattice q-grams plus those of the first
-    // steps (first_steps_eval reads the q-grams ending at a_k - q and a_k - q + S)
+    // steps (first_steps_eval reads the q-grams ending at a_k - q, a_k - q + S and
+    // a_k - 2q + S, all inside this range)
     const uint32_t a0 = p.m - 1 + g.k0 * p.S;
     g.first = a0 + 1 >= 2 * p.q ? a0 + 1 - 2 * p.q : 0u;
     const uint32_t alast = p.m - 1 + (g.k1 - 1) * p.S;
@@ -781,6 +856,189 @@ __device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint3
         }
     }
     cp_async_commit();   // one group per issue (possibly empty) keeps the count uniform
+}
+
+// ------------------------------------------------------------------ fused epilogue
+// Every search kernel ends here: the last CTA to finish publishes the
+// occurrence count to the host (mapped pinned memory), resets the counter words for the
+// next call, and orders up to epi_cap positions into the caller's int64 buffer in its
+// own (now idle) shared memory.  One kernel launch per hc_search in the common case;
+// the host orders only what the epilogue could not (hc_finish.cu).
+
+// Block-wide min / max / sum (blockDim.x a multiple of 32; `tmp` >= 32 shared words).
+__device__ __forceinline__ uint32_t block_min(uint32_t v, uint32_t *tmp) {
+    v = __reduce_min_sync(HC_FULL, v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) tmp[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = tmp[0];
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) r = min(r, tmp[w]);
+    return r;
+}
+__device__ __forceinline__ uint32_t block_max(uint32_t v, uint32_t *tmp) {
+    v = __reduce_max_sync(HC_FULL, v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) tmp[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = tmp[0];
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) r = max(r, tmp[w]);
+    return r;
+}
+// In-place exclusive scan of c[0..NB) (NB a power of two, 32 <= NB <= 32 * blockDim.x)
+// by the whole block; every thread gets the total.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t *c, uint32_t NB, uint32_t *tmp) {
+    const uint32_t T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t per = (NB + T - 1) / T;            // counters per thread (consecutive)
+    const uint32_t b0 = t * per;
+    uint32_t loc = 0;
+    for (uint32_t i = 0; i < per; ++i)
+        if (b0 + i < NB) loc += c[b0 + i];
+    uint32_t incl = loc;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(HC_FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    __syncthreads();
+    if (lane == 31) tmp[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0, total = 0;
+    for (uint32_t w = 0; w < T / 32; ++w) {
+        const uint32_t x = tmp[w];
+        if (w < warp) wbase += x;
+        total += x;
+    }
+    uint32_t run = wbase + incl - loc;
+    for (uint32_t i = 0; i < per; ++i)
+        if (b0 + i < NB) {
+            const uint32_t x = c[b0 + i];
+            c[b0 + i] = run;
+            run += x;
+        }
+    __syncthreads();
+    return total;
+}
+
+// Orders `count` distinct positions pos[0..count) (2 <= count) into dst[0..k) ascending,
+// in shared memory `sm` (>= epi_bytes(count) bytes), by the whole block.  Small sets by
+// rank counting; larger ones by a bucket pass on the positions' offset from their
+// minimum (power-of-two buckets, count/2 to count of them) and rank counting inside
+// each bucket.  Returns false when some bucket holds more than kEpiBucketMax keys
+// (strongly clustered positions): the host then orders them (nothing is assumed of dst).
+constexpr uint32_t kEpiRankMax = 256;
+constexpr uint32_t kEpiBucketMax = 64;
+static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t count, int64_t *dst, uint32_t k,
+                                         uint8_t *sm) {
+    const uint32_t T = blockDim.x, t = threadIdx.x;
+    uint32_t *tmp = reinterpret_cast<uint32_t *>(sm);            // 64 words
+    uint32_t *ks = tmp + 64;                                     // count keys (16-B aligned)
+    // all keys to shared memory with 16-byte cp.async copies: one L2 round trip (the
+    // scratch is 16-byte aligned and has >= 3 words of slack past any count)
+    for (uint32_t i = 4 * t; i < count; i += 4 * T)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(ks + i)), "l"(pos + i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (count <= kEpiRankMax) {
+        for (uint32_t i = t; i < count; i += T) {
+            const uint32_t key = ks[i];
+            uint32_t r = 0;
+            for (uint32_t j = 0; j < count; ++j) r += ks[j] < key;
+            if (r < k) dst[r] = static_cast<int64_t>(key);
+        }
+        return true;
+    }
+    uint32_t NB = 32;
+    while (NB < 2048 && 2 * NB < count) NB <<= 1;                // count/2 <= NB < count
+    uint32_t *c = ks + ((count + 3) & ~3u);                      // NB bucket counters
+    uint32_t *k2 = c + NB;                                       // keys grouped by bucket
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (uint32_t i = t; i < count; i += T) {
+        const uint32_t key = ks[i];
+        lo = min(lo, key);
+        hi = max(hi, key);
+    }
+    for (uint32_t i = t; i < NB; i += T) c[i] = 0;
+    lo = block_min(lo, tmp);
+    hi = block_max(hi, tmp + 32);
+    // bucket = (key - lo) >> sh with (hi - lo) >> sh < NB
+    uint32_t sh = 0;
+    while (((hi - lo) >> sh) >= NB) ++sh;
+    for (uint32_t i = t; i < count; i += T) atomicAdd(&c[(ks[i] - lo) >> sh], 1u);
+    __syncthreads();
+    uint32_t big = 0;
+    for (uint32_t i = t; i < NB; i += T) big |= c[i] > kEpiBucketMax;
+    if (__syncthreads_or(big)) return false;
+    block_exclusive_scan(c, NB, tmp);                            // c[b] = start of bucket b
+    for (uint32_t i = t; i < count; i += T) {
+        const uint32_t key = ks[i];
+        k2[atomicAdd(&c[(key - lo) >> sh], 1u)] = key;           // c[b] ends at bucket b's end
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < count; i += T) {
+        const uint32_t key = k2[i];
+        const uint32_t b = (key - lo) >> sh;
+        const uint32_t b_lo = b ? c[b - 1] : 0u, b_hi = c[b];
+        uint32_t r = b_lo;
+        for (uint32_t j = b_lo; j < b_hi; ++j) r += k2[j] < key;
+        if (r < k) dst[r] = static_cast<int64_t>(key);
+    }
+    return true;
+}
+
+// True in every thread of the last CTA of the grid to get here.  Every thread fences its
+// own position stores and counter atomics before the CTA takes its ticket, and the last
+// CTA fences again before reading what the others wrote.
+__device__ __forceinline__ bool cta_is_last(uint32_t *ticket) {
+    __shared__ uint32_t s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    const bool last = s_last != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// The last CTA's work for one search: publish, order when possible, reset the counters.
+// `smem` is the CTA's dynamic shared memory (idle by now), `smem_bytes` its size.
+__device__ __forceinline__ void publish_search(uint32_t *counter, const uint32_t *out, uint32_t cap,
+                                               uint32_t *host_count, int64_t *dst, uint32_t k_out,
+                                               uint32_t epi_cap, uint8_t *smem, bool fault) {
+    const uint32_t count = *reinterpret_cast<volatile uint32_t *>(counter);
+    bool ordered = count == 0 || dst == nullptr || k_out == 0;
+    if (!ordered && count <= cap && count <= epi_cap) {
+        if (count == 1) {
+            if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(__ldcg(out));
+            ordered = true;
+        } else {
+            ordered = block_order(out, count, dst, k_out, smem);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (kInstrument && fault && ordered && count > 0 && dst && k_out)
+            dst[0] += 1;                           // fault-injection hook (tests only)
+        counter[0] = 0;
+        counter[1] = 0;
+        host_count[1] = ordered ? 1u : 0u;
+        host_count[0] = count;
+    }
+}
+
+// Largest count the epilogue orders in `smem_bytes` of dynamic shared memory.
+inline uint32_t epi_cap_for(int smem_bytes) {
+    uint32_t c = smem_bytes > 544 ? (static_cast<uint32_t>(smem_bytes) - 544u) / 12u : 0u;
+    return c < kSmallSort ? c : kSmallSort;
+}
+
+// Single-pattern kernels: the epilogue of search p (call from every thread at the end).
+__device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem) {
+    if (!cta_is_last(p.counter + 2)) return;
+    publish_search(p.counter, p.out, p.cap, p.host_count, p.dst, p.k_out, p.epi_cap, smem,
+                   p.debug == 9);
+    __syncthreads();
+    if (threadIdx.x == 0) p.counter[2] = 0;
 }
 
 // ------------------------------------------------------------------ launch helpers

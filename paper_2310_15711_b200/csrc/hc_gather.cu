@@ -7,17 +7,23 @@
 namespace hc {
 
 struct GatherLayout {
-    uint32_t f_off, x_off, q_off, q2_off, wbuf_off, total;
+    uint32_t f_off, x_off, bits_off, q_off, q2_off, wbuf_off, bar_off, total;
+    uint32_t f_bytes, x_bytes, bits_words;   // bulk-copied F and x, bitmap words
 };
 __host__ __device__ inline GatherLayout gather_layout(uint32_t alpha, uint32_t m,
                                                       uint32_t nwarps) {
     GatherLayout L;
+    L.f_bytes = round_up((1u << alpha) * 4u, 16);
+    L.x_bytes = round_up(m + 8, 16);
+    L.bits_words = (1u << alpha) / 32 > 4 ? (1u << alpha) / 32 : 4u;
     L.f_off = 0;
-    L.x_off = round_up((1u << alpha) * 4u, 16);
-    L.q_off = L.x_off + round_up(m + 8, 16);
+    L.x_off = L.f_bytes;
+    L.bits_off = L.x_off + L.x_bytes;
+    L.q_off = L.bits_off + 4 * L.bits_words;
     L.q2_off = L.q_off + nwarps * kWarpBuf * 4u;
     L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
-    L.total = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    L.bar_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
+    L.total = L.bar_off + 16;
     return L;
 }
 
@@ -25,38 +31,116 @@ int gather_smem_bytes(uint32_t alpha, uint32_t m) {
     return static_cast<int>(gather_layout(alpha, m, kGatherThreads / 32).total);
 }
 
+// One warp's lattice loop.  Chunk c holds the lattice points [c*32L, (c+1)*32L); lane l
+// takes points c*32L + u*32 + l, u < L.  The L q-gram loads of a chunk are issued
+// together (one DRAM round trip per chunk instead of one per round), and the next
+// chunk's loads are issued before this chunk's survivors are handed to the sink
+// (first steps / phase B round trips), so they overlap.  The first chunk's loads are
+// issued before the table load (`W` comes in loaded).
+template <int Q, int SH, int L, class Sink>
+__device__ __forceinline__ void gather_loop(const KParams &p, const GlobalText &txt, const FBits &fb,
+                                            uint32_t c, uint32_t total_warps, uint32_t lane,
+                                            uint64_t (&W)[4], Sink &sink, uint64_t *bar,
+                                            bool &ready) {
+    const uint32_t step = 32 * p.S;
+    while (c < p.nchunks) {
+        const uint32_t k0 = c * 32 * L;
+        const uint32_t pos0 = p.m - 1 + (k0 + lane) * p.S;
+        bool pass[L];
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < L; ++u) {
+            pass[u] = k0 + u * 32 + lane < p.K && fb.pass(qhash<Q, SH>(W[u], p.mask));   // l.4-6
+            any |= pass[u];
+        }
+        c += total_warps;
+        if (c < p.nchunks) {                       // next chunk's loads, before the survivors
+            const uint32_t kn = c * 32 * L + lane;
+#pragma unroll
+            for (int u = 0; u < L; ++u)
+                W[u] = kn + u * 32 < p.K ? end8<Q>(txt, p.m - 1 + (kn + u * 32) * p.S) : 0ull;
+        }
+        if (__any_sync(HC_FULL, any)) {
+            if (!ready) {                          // F and x (TMA bulk copy) are needed now
+                mbar_wait(bar, 0);
+                ready = true;
+            }
+#pragma unroll
+            for (int u = 0; u < L; ++u) {
+                const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
+                if (bm) sink(bm, pass[u], pos0 + u * step);
+            }
+        }
+    }
+}
+
+// Table load: thread 0 starts ONE TMA bulk copy of F and x (complete_tx on an mbarrier),
+// the filter bitmap (2^alpha bits) is loaded by the threads in one round trip, and the
+// lattice filter runs on the bitmap while F is still in flight; a warp waits for F only
+// when it first has survivors.  Every warp waits before the end, so the copy has landed
+// before the epilogue reuses the shared memory.
 template <int Q, int SH>
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kGatherThreads / 32;
-    const GatherLayout L = gather_layout(p.alpha, p.m, NW);
-    uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
-    uint8_t *sx = smem + L.x_off;
+    const GatherLayout Lo = gather_layout(p.alpha, p.m, NW);
+    uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + Lo.f_off);
+    uint8_t *sx = smem + Lo.x_off;
+    uint32_t *sbits = reinterpret_cast<uint32_t *>(smem + Lo.bits_off);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Lo.bar_off);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (kInstrument && tid == 0) trace_cta(p, 0);
-    pdl_launch_dependents();
-    load_table(p, sFp, sx);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, Lo.f_bytes + Lo.x_bytes);
+        bulk_g2s(smem_u32(sFp), p.F, Lo.f_bytes, bar);
+        bulk_g2s(smem_u32(sx), p.x, Lo.x_bytes, bar);   // x is followed by >= 24 zero bytes
+    }
+    // the filter bitmap first (its loads must not queue behind the lattice's DRAM misses)
+    uint32_t bw = 0;
+    if (tid < Lo.bits_words) bw = __ldg(p.Fbits + tid);
+    const GlobalText txt{p.y};
+    const uint32_t total_warps = gridDim.x * NW;
+    const uint32_t c0 = blockIdx.x * NW + warp;
+    const uint32_t L = p.seg_per_chunk / 32;   // lattice points per lane per chunk: 1, 2 or 4
+    // then the first chunk's lattice loads (they overlap the bitmap's round trip)
+    uint64_t W[4] = {0ull, 0ull, 0ull, 0ull};
+    if (c0 < p.nchunks) {
+        const uint32_t kn = c0 * p.seg_per_chunk + lane;
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u)
+            if (u < L && kn + u * 32 < p.K) W[u] = end8<Q>(txt, p.m - 1 + (kn + u * 32) * p.S);
+    }
+    if (tid < Lo.bits_words) sbits[tid] = bw;
+    for (uint32_t w = tid + blockDim.x; w < Lo.bits_words; w += blockDim.x) sbits[w] = __ldg(p.Fbits + w);
     if (tid == 0) s_params[0] = p;
     __syncthreads();
     const FTable sF{fence_value(smem_u32(sFp))};
-    WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
-    const GlobalText txt{p.y};
+    const FBits fb{fence_value(smem_u32(sbits))};
+    WarpOut wo{reinterpret_cast<uint32_t *>(smem + Lo.wbuf_off) + warp * kWarpBuf, 0u};
     WarpQueueSink<Q, SH, GlobalText> sink{p, txt, sF, sx,
-                                          reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kWarpBuf,
-                                          reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
+                                          reinterpret_cast<uint32_t *>(smem + Lo.q_off) + warp * kWarpBuf,
+                                          reinterpret_cast<uint32_t *>(smem + Lo.q2_off) + warp * kWarpBuf,
                                           0u, 0u, wo, lane};
-    const uint32_t total_warps = gridDim.x * NW;
-    if (kInstrument && warp == 0 && lane == 0) trace_event(p, 0, 0);          // table loaded
-    for (uint32_t c = blockIdx.x * NW + warp; c < p.nchunks; c += total_warps) {
-        const uint32_t seg_lo = c * p.seg_per_chunk;
-        const uint32_t seg_hi = min(seg_lo + p.seg_per_chunk, p.K);
-        filter_lattice<Q, SH>(p, txt, sF, seg_lo, seg_hi, lane, sink);
-    }
-    if (kInstrument && warp == 0 && lane == 0) trace_event(p, 0, 1);          // lattice filtered
+    bool ready = false;
+    if (kInstrument && lane == 0) trace_event(p, warp, 0);          // bitmap loaded
+    if (L >= 4)
+        gather_loop<Q, SH, 4>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
+    else if (L == 2)
+        gather_loop<Q, SH, 2>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
+    else
+        gather_loop<Q, SH, 1>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
+    if (!ready) mbar_wait(bar, 0);
+    if (kInstrument && lane == 0) trace_event(p, warp, 1);          // lattice filtered
     sink.drain();
-    if (kInstrument && warp == 0 && lane == 0) trace_event(p, 0, 2);          // survivors done
+    if (kInstrument && lane == 0) trace_event(p, warp, 2);          // survivors done
     wo.flush(p, lane);
+    if (kInstrument && lane == 0) trace_event(p, warp, 3);          // flushed
     if (kInstrument && lane == 0) trace_cta(p, 1);   // last warp to get here wins
+    __syncthreads();
+    if (tid == 0) mbar_inval(bar);                 // the epilogue may reuse this memory
+    search_epilogue(p, smem);
 }
 
 template <int Q, int SH>
@@ -72,6 +156,7 @@ cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int c
     const int smem = gather_smem_bytes(p.alpha, p.m);
     const long ctas = (static_cast<long>(p.nchunks) + kGatherThreads / 32 - 1) / (kGatherThreads / 32);
     KParams a = p;
+    a.epi_cap = epi_cap_for(smem);
     void *args[] = {&a};
     return launch_kernel(reinterpret_cast<const void *>(kern), args, kGatherThreads, smem, ctas,
                          max_ctas, ctas_per_sm, st, li);

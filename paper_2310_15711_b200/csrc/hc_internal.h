@@ -13,7 +13,8 @@ struct KParams {
     const uint8_t *y;    // text, device, any alignment
     uint32_t n;          // text length (n >= m, n <= HC_MAX_TEXT)
     const uint32_t *F;   // filter table, device, 2^alpha words
-    const uint8_t *x;    // pattern, device
+    const uint32_t *Fbits;  // filter bitmap, device, 2^alpha bits (bit v = F[v] != 0), >= 16 B
+    const uint8_t *x;    // pattern, device, followed by >= 24 zero bytes (16-byte aligned)
     uint32_t m, q, s, mask, hv;
     uint32_t S;          // shift m - q + 1: also the segment length
     uint32_t alpha;
@@ -34,7 +35,15 @@ struct KParams {
     // output
     uint32_t *out;       // positions (window starts), unordered; NULL = count only
     uint32_t cap;        // capacity of out
-    uint32_t *counter;   // [0] = total occurrences (may exceed cap)
+    uint32_t *counter;   // kCtr words: [0] = total occurrences (may exceed cap), [1] = staged
+                         // tile counter, [2] = CTAs done (epilogue ticket); zero between calls
+    // fused epilogue (the last CTA to finish): count publication + ordering
+    uint32_t *host_count;  // mapped pinned [2]: count, then 1 if the positions were ordered
+                           // into dst by the epilogue (else the host orders them)
+    int64_t *dst;        // caller's pos_out (device), NULL = count only
+    uint32_t k_out;      // min(max_out, windows)
+    uint32_t epi_cap;    // largest count the epilogue orders in its CTA's shared memory
+    uint32_t nbits;      // positions are < 2^nbits
     uint32_t debug;      // 1: staged kernel skips the search (pipeline measurement only)
     uint32_t tma_chunk;  // staged: split each tile's bulk copy into pieces of this size (0 = one)
     unsigned long long *trace;  // staged: per-(CTA, tile) %globaltimer events (debugging), or NULL
@@ -52,7 +61,11 @@ struct MParams {
     uint32_t *counter[kMaxPatterns];
     uint32_t *out[kMaxPatterns];
     uint32_t cap[kMaxPatterns];
+    uint32_t *host_count[kMaxPatterns];
+    int64_t *dst[kMaxPatterns];
+    uint32_t k_out[kMaxPatterns];
 };
+constexpr int kCtr = 8;   // counter words per search (KParams::counter)
 
 struct LaunchInfo {
     int grid = 0, block = 0, smem = 0;
@@ -71,16 +84,21 @@ int mstream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t 
                        uint32_t bufs);
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
-// One CTA after the search kernel: count -> host_count (mapped pinned), counter reset,
-// ordering of <= kSmallSort positions into dst (first min(count, max_out), int64).
-cudaError_t launch_finish(uint32_t *counter, const uint32_t *pos, uint32_t cap, int64_t *dst,
-                          uint32_t max_out, uint32_t n_bound, uint32_t *host_count_dev,
-                          cudaStream_t st,
-                          unsigned long long *trace = nullptr);
-// Ordering of count > kSmallSort positions (CUB radix sort), first k written as int64.
-cudaError_t sort_large(const uint32_t *pos, uint32_t count, uint32_t n_bound, int64_t *dst,
-                       uint32_t k, cudaStream_t st, int *launches);
+// Ordering of `count` distinct positions (u32, unordered) into dst: the smallest k,
+// ascending, as int64.  Used when the search kernel's epilogue did not order them
+// (count above its shared-memory capacity, or skewed).  count <= kSmallSort: one CTA
+// (bucket pass / block radix sort); larger: an n-bit bitmap and a popcount-prefix
+// compaction (no comparison sort).  Adds the launches it made to *launches.
+cudaError_t order_positions(const uint32_t *pos, uint32_t count, uint32_t n, int64_t *dst,
+                            uint32_t k, cudaStream_t st, int *launches);
 constexpr uint32_t kSmallSort = 8192;
+inline uint32_t bits_for(uint32_t n) {   // positions < n fit in bits_for(n) bits
+    uint32_t b = 1;
+    while (b < 32 && (static_cast<uint64_t>(1) << b) < n) ++b;
+    return b;
+}
+// shared-memory bytes the epilogue needs to order `count` positions (keys + bucket array)
+constexpr uint32_t epi_bytes(uint32_t count) { return 12u * count + 544u; }
 
 int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t stages,
                       uint32_t slot_bytes, uint32_t nbox);

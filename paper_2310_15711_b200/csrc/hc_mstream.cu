@@ -252,6 +252,15 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
         sink.drain();
         wo.flush(pp, lane);
     }
+    // fused epilogue: the last CTA publishes and orders every pattern's positions
+    if (cta_is_last(mp.counter[0] + 2)) {
+        for (uint32_t i = 0; i < P; ++i) {
+            publish_search(mp.counter[i], mp.out[i], mp.cap[i], mp.host_count[i], mp.dst[i],
+                           mp.k_out[i], p.epi_cap, smem, p.debug == 9);
+            __syncthreads();
+        }
+        if (tid == 0) mp.counter[0][2] = 0;
+    }
 }
 
 template <int Q, int SH>
@@ -268,6 +277,7 @@ cudaError_t launch_mstream(const KParams &p, const MParams &mp, cudaStream_t st,
     const int smem = mstream_smem_bytes(p.alpha, p.m, p.stage_bytes, nw, mp.npat, p.stages);
     const long ctas = (p.nchunks + nw - 1) / nw;
     KParams a = p;
+    a.epi_cap = epi_cap_for(smem);
     MParams b = mp;
     void *args[] = {&a, &b};
     return launch_kernel(reinterpret_cast<const void *>(kern), args, static_cast<int>(32 * nw), smem,

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kStreamMaxThreads) shc_kernel(const KParams p)
         bsel = bn;
     }
     cp_async_wait<0>();
+    search_epilogue(p, smem);
 }
 
 template <int Q, int SH>
@@ -133,6 +134,7 @@ cudaError_t launch_shc(const KParams &p, cudaStream_t st, int max_ctas, int ctas
     const int smem = shc_smem_bytes(p.alpha, p.m, p.stage_bytes, p.slot_bytes, nw);
     const long ctas = (p.nchunks + nw - 1) / nw;
     KParams a = p;
+    a.epi_cap = epi_cap_for(smem);
     void *args[] = {&a};
     return launch_kernel(reinterpret_cast<const void *>(kern), args, static_cast<int>(32 * nw), smem,
                          ctas, max_ctas, ctas_per_sm, st, li);

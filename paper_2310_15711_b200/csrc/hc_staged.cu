@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
     }
     wo.flush(p, lane);
     if (kInstrument && lane == 0) trace_cta(p, 1);   // last warp to get here wins
+    search_epilogue(p, smem);
 }
 
 template <int Q, int SH>
@@ -381,6 +382,7 @@ cudaError_t launch_staged(const KParams &p, cudaStream_t st, int max_ctas, int c
     if (!kern) return cudaErrorInvalidValue;
     const int smem = staged_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, p.slot_bytes, p.nbox);
     KParams a = p;
+    a.epi_cap = epi_cap_for(smem);
     void *args[] = {&a};
     return launch_kernel(reinterpret_cast<const void *>(kern), args, kStagedThreads, smem,
                          static_cast<long>(p.ntiles), max_ctas, ctas_per_sm, st, li);

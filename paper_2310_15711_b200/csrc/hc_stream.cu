@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(kStreamMaxThreads) stream_kernel(const KParams
     sink.drain();
     wo.flush(p, lane);
     if (kInstrument && lane == 0) trace_cta(p, 1);
+    search_epilogue(p, smem);
 }
 
 template <int Q, int SH>
@@ -272,6 +273,7 @@ cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int c
     const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, nw);
     const long ctas = (p.nchunks + nw - 1) / nw;
     KParams a = p;
+    a.epi_cap = epi_cap_for(smem);
     void *args[] = {&a};
     return launch_kernel(reinterpret_cast<const void *>(kern), args, static_cast<int>(32 * nw), smem,
                          ctas, max_ctas, ctas_per_sm, st, li);

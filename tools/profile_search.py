@@ -99,16 +99,23 @@ def main():
                   + (f" phaseB iters={st['dbg'][0]} calls={st['dbg'][1]}" if args.debug == 5 else ""),
                   flush=True)
             if args.trace and r == args.reps - 1 and st["path"] == 2:
+                # gather: per-warp events (trace_tiles >= 8): table loaded, filtered, drained, flushed
                 import numpy as np
-                g = st["grid"]
-                a = tr[:g * args.trace * 4].view(g, args.trace, 4)[:, 0, :3].cpu().numpy().astype(np.float64)
-                ce = tr[g * args.trace * 4: g * args.trace * 4 + 2 * g].view(g, 2).cpu().numpy().astype(np.float64)
+                g, T = st["grid"], args.trace
+                a = tr[:g * T * 4].view(g, T, 4)[:, :8, :].cpu().numpy().astype(np.float64)
+                ce = tr[g * T * 4: g * T * 4 + 2 * g].view(g, 2).cpu().numpy().astype(np.float64)
                 t0 = ce[:, 0].min()
                 rel = lambda v: (v - t0) / 1e3
-                for nm, v in [("entry", ce[:, 0]), ("table loaded", a[:, 0]), ("filtered", a[:, 1]),
-                              ("survivors done", a[:, 2]), ("exit", ce[:, 1])]:
-                    r_ = rel(v)
-                    print(f"  gather warp0 {nm}: p50 {np.median(r_):.2f} p90 {np.percentile(r_, 90):.2f} max {r_.max():.2f} us")
+                for k_, nm in enumerate(["table loaded", "filtered", "drained", "flushed"]):
+                    r_ = rel(a[:, :, k_]).ravel()
+                    print(f"  gather warps {nm}: p10 {np.percentile(r_, 10):.2f} p50 {np.median(r_):.2f} "
+                          f"p90 {np.percentile(r_, 90):.2f} p99 {np.percentile(r_, 99):.2f} max {r_.max():.2f} us")
+                d = rel(a[:, :, 2]) - rel(a[:, :, 1])
+                print(f"  drain time per warp: p50 {np.median(d):.2f} p99 {np.percentile(d, 99):.2f} max {d.max():.2f}")
+                r_ = rel(ce[:, 1])
+                print(f"  CTA exit: p50 {np.median(r_):.2f} p90 {np.percentile(r_, 90):.2f} max {r_.max():.2f} us")
+                worst = np.unravel_index(np.argmax(a[:, :, 3]), a[:, :, 3].shape)
+                print(f"  slowest warp (cta {worst[0]}, warp {worst[1]}):", np.round(rel(a[worst[0], worst[1]]), 2))
             elif args.trace and r == args.reps - 1:
                 analyze_trace(tr, st["grid"], args.trace, args.stages or 3)
                 if args.debug == 11:
