@@ -101,8 +101,10 @@ typedef enum hc_path {
     HC_PATH_STAGED = 1, /* text tiles staged in shared memory by TMA bulk copies */
     HC_PATH_GATHER = 2, /* no staging: lanes read only the q-grams they hash, from global memory */
     HC_PATH_STREAM = 3, /* per-warp chunks staged in shared memory by 16-byte cp.async copies */
-    HC_PATH_SHC = 4     /* Sentinel Hash Chain (Fig. 5 right): per-lane ranges copied into shared-
+    HC_PATH_SHC = 4,    /* Sentinel Hash Chain (Fig. 5 right): per-lane ranges copied into shared-
                            memory boxes followed by a copy of x, SHC's fast loop per lane */
+    HC_PATH_SCAN = 5    /* hash every position of staged pieces once into filter / link bitmaps,
+                           then Fig. 5's loop per segment with O(1) walks (walk-heavy texts) */
 } hc_path;
 
 typedef struct hc_search_opts {

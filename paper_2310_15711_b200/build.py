@@ -23,7 +23,7 @@ LIB = os.path.join(HERE, "libhc.so")
 LIB_INSTR = os.path.join(HERE, "libhc_instr.so")
 OBJ = os.path.join(ROOT, "build_obj")
 SOURCES = ["hc_api.cpp", "hc_launch.cu", "hc_stream.cu", "hc_gather.cu", "hc_mstream.cu",
-           "hc_finish.cu", "hc_shc.cu", "hc_staged.cu"]
+           "hc_finish.cu", "hc_shc.cu", "hc_staged.cu", "hc_scan.cu"]
 HEADERS = ["hc_internal.h", "hc_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

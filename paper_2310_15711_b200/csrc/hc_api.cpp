@@ -257,6 +257,7 @@ cudaError_t launch_search(int path, const hc::KParams &p, cudaStream_t st, const
     case HC_PATH_STAGED: return hc::launch_staged(p, st, o.max_ctas, o.ctas_per_sm, li);
     case HC_PATH_STREAM: return hc::launch_stream(p, st, o.max_ctas, o.ctas_per_sm, li);
     case HC_PATH_SHC: return hc::launch_shc(p, st, o.max_ctas, o.ctas_per_sm, li);
+    case HC_PATH_SCAN: return hc::launch_scan(p, st, o.max_ctas, o.ctas_per_sm, li);
     default: return hc::launch_gather(p, st, o.max_ctas, o.ctas_per_sm, li);
     }
 }
@@ -288,7 +289,13 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
     p.trace_tiles = o.trace_tiles > 0 ? static_cast<uint32_t>(o.trace_tiles) : 0u;
 
     path = o.path;
-    if (path == HC_PATH_AUTO) path = S <= kStagedMaxShift ? HC_PATH_STREAM : HC_PATH_GATHER;
+    if (path == HC_PATH_AUTO) {
+        path = S <= kStagedMaxShift ? HC_PATH_STREAM : HC_PATH_GATHER;
+        // the gather search may give up on walk-heavy text and be re-run on the scan path
+        // (hc_gather.cu), when the scan path can take this pattern
+        p.allow_abort = path == HC_PATH_GATHER &&
+                        hc::scan_smem_bytes(p.alpha, m, q, 0) <= smem_budget(h->device);
+    }
     if (path == HC_PATH_STAGED) {
         uint32_t stage = o.tile_bytes > 0 ? static_cast<uint32_t>(o.tile_bytes) : kDefaultStageBytes;
         // at least 32 segments (one per lane of a warp) per tile
@@ -361,6 +368,12 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         if (hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) > smem_budget(h->device))
             return HC_EINVAL;   // m too long for per-lane boxes
         p.block_warps = nw;
+    }
+    if (path == HC_PATH_SCAN) {
+        // pieces of window ends staged with their (m-1)-byte halo (hc_scan.cu)
+        p.nchunks = 0;
+        if (hc::scan_smem_bytes(p.alpha, m, q, 0) > smem_budget(h->device))
+            return HC_EINVAL;   // pattern too long for the staged pieces
     }
     if (path == HC_PATH_GATHER) {
         // lattice points per lane per chunk (1, 2 or 4; the chunk's loads go out together):
@@ -705,6 +718,16 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         }
         const volatile uint32_t *hcnt = sc->host_count;
         count = hcnt[0];
+        if (hcnt[1] == 2u) {
+            // walk-heavy text: the gather search gave up; the scan path hashes every
+            // q-gram once (hc_scan.cu) and returns exactly the same result
+            hc_search_opts os = o;
+            os.path = HC_PATH_SCAN;
+            const int rc = setup_search(h, y_dev, nn, os, p, path);
+            if (rc != HC_OK) return fail(rc);
+            ++reruns;
+            continue;
+        }
         const bool ordered = hcnt[1] != 0;
         if (HC_INSTRUMENT && o.debug == 5 && stats) {
             cudaMemcpy(stats->dbg, sc->buf + 4, 8, cudaMemcpyDeviceToHost);
@@ -921,15 +944,18 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
     int reruns = 0;
     for (size_t i = 0; i < npat; ++i) {
         const uint32_t c = reinterpret_cast<volatile uint32_t *>(r->hcounts)[2 * i];
-        const bool ordered = reinterpret_cast<volatile uint32_t *>(r->hcounts)[2 * i + 1] != 0;
+        const uint32_t flag = reinterpret_cast<volatile uint32_t *>(r->hcounts)[2 * i + 1];
+        const bool ordered = flag == 1u;
+        const bool gave_up = flag == 2u;   // walk-heavy text: the count is not known
         counts[i] = c;
         const size_t mo = max_out ? max_out[i] : 0;
         const bool want_pos = pos_out && pos_out[i] && mo > 0;
-        if (want_pos && c > 0 && (c > caps[i] || !ordered)) {
+        if (gave_up || (want_pos && c > 0 && (c > caps[i] || !ordered))) {
             hc_search_opts orr = o;
             orr.time_kernel = 0;
             hc_search_stats rs{};
-            const int64_t c2 = hc_search_ex(hs[i], y_dev, n, pos_out[i], mo, stream, &orr, &rs);
+            const int64_t c2 = hc_search_ex(hs[i], y_dev, n, want_pos ? pos_out[i] : nullptr,
+                                            want_pos ? mo : 0, stream, &orr, &rs);
             if (c2 < 0) return bail(static_cast<int>(c2));
             launches += rs.launches;
             counts[i] = c2;

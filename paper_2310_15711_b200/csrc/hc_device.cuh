@@ -657,6 +657,13 @@ __device__ __forceinline__ bool first_steps_eval(const KParams &p, const T &txt,
 // time through first_steps_eval; the segments that continue go to a second queue
 // (q2, window ends) that runs phase B whenever 32 are queued (both queues may span
 // chunks, since the survivors read global memory).
+// Walk-heavy text (KParams::allow_abort, gather path): when more than half of a warp's
+// first lattice survivors walk on past their first link test, Fig. 5's loop would
+// re-hash most q-grams many times over (the stress config C5: ~7 hashes per text byte);
+// the warp raises the give-up flag before any walk runs, every warp stops at its next
+// chunk, and the host re-runs the search on the scan path, which hashes every q-gram
+// once (hc_scan.cu).
+constexpr uint32_t kAbortMinSurvivors = 32;
 template <int Q, int SH, class T, class FT = FTable>
 struct WarpQueueSink {
     const KParams &p;
@@ -668,6 +675,9 @@ struct WarpQueueSink {
     WarpOut &wo;
     uint32_t lane;
     uint32_t pi = 0;       // pattern index (launch parameters s_params[pi])
+    uint32_t n_surv = 0;   // lattice survivors through first steps (warp-uniform)
+    uint32_t n_walk = 0;   // ... of which the walk went on past its first link test
+    bool gave_up = false;  // allow_abort: walk-heavy text detected (see hc_gather.cu)
     __device__ __forceinline__ void steps(uint32_t c) {  // first steps of q1[0..c) -> q2
         const bool act = lane < c;
         steps_e(act, act ? q1[lane] : 0u);
@@ -680,6 +690,15 @@ struct WarpQueueSink {
         uint32_t start;
         const bool keep = first_steps_eval<Q, SH>(p, t2, sF, act, e, start);
         const uint32_t bm = __ballot_sync(HC_FULL, keep);
+        n_surv += __popc(__ballot_sync(HC_FULL, act));
+        n_walk += __popc(__ballot_sync(HC_FULL, keep && start == e));
+        if (p.allow_abort && n_surv >= kAbortMinSurvivors && 2 * n_walk > n_surv) {
+            // walk-heavy text: give up before the walks (phase B) cost anything
+            if (lane == 0) *reinterpret_cast<volatile uint32_t *>(p.counter + 3) = 1u;
+            gave_up = true;
+            n1 = n2 = 0;
+            return;
+        }
         if (keep) q2[n2 + __popc(bm & lanemask_lt())] = start;
         n2 += __popc(bm);
         if (n2 >= 32) {
@@ -694,6 +713,7 @@ struct WarpQueueSink {
         }
     }
     __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t e) {
+        if (gave_up) return;
         if (pass) q1[n1 + __popc(bm & lanemask_lt())] = e;
         n1 += __popc(bm);
         if (n1 >= 32) {
@@ -827,14 +847,17 @@ __device__ __forceinline__ StreamChunk stream_chunk(const KParams &p, uint32_t c
 // Issues chunk c's copies into the buffer at shared address `buf` (one warp).  The
 // 16-byte words wholly inside y are copied with cp.async; the bytes of the partial
 // words at the two ends of an unaligned text are stored directly (first/last chunk).
-__device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint32_t buf,
-                                             uint32_t lane) {
-    if (c < p.nchunks) {
-        const StreamChunk g = stream_chunk(p, c);
+// Copies text bytes [first, last] into the buffer at shared address `buf` (one warp):
+// the 16-byte words wholly inside y with cp.async, the bytes of the partial words at the
+// two ends of an unaligned text directly.  Text byte t lands at buf + (y + t) % 16 +
+// (t - first).  One commit group per call (possibly empty).
+__device__ __forceinline__ void issue_range(const KParams &p, bool any, uint32_t first, uint32_t last,
+                                            uint32_t buf, uint32_t lane) {
+    if (any) {
         const uintptr_t y = reinterpret_cast<uintptr_t>(p.y);
-        const uintptr_t A = (y + g.first) & ~static_cast<uintptr_t>(15);
+        const uintptr_t A = (y + first) & ~static_cast<uintptr_t>(15);
         const uint32_t nbytes =
-            static_cast<uint32_t>(((y + g.last + 16) & ~static_cast<uintptr_t>(15)) - A);
+            static_cast<uint32_t>(((y + last + 16) & ~static_cast<uintptr_t>(15)) - A);
         const uintptr_t ye = y + p.n;
         if (A >= y && A + nbytes <= ye) {               // warp-uniform: interior chunk
             const uint8_t *src = reinterpret_cast<const uint8_t *>(A);
@@ -856,6 +879,12 @@ __device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint3
         }
     }
     cp_async_commit();   // one group per issue (possibly empty) keeps the count uniform
+}
+__device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint32_t buf,
+                                             uint32_t lane) {
+    StreamChunk g{0, 0, 0, 0};
+    if (c < p.nchunks) g = stream_chunk(p, c);
+    issue_range(p, c < p.nchunks, g.first, g.last, buf, lane);
 }
 
 // ------------------------------------------------------------------ fused epilogue
@@ -1035,6 +1064,16 @@ inline uint32_t epi_cap_for(int smem_bytes) {
 // Single-pattern kernels: the epilogue of search p (call from every thread at the end).
 __device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem) {
     if (!cta_is_last(p.counter + 2)) return;
+    if (*reinterpret_cast<volatile uint32_t *>(p.counter + 3)) {
+        // the search gave up (walk-heavy text, see gather_kernel): the host re-runs it on
+        // the scan path; nothing of this run is published but the verdict
+        if (threadIdx.x == 0) {
+            p.counter[0] = p.counter[1] = p.counter[2] = p.counter[3] = 0;
+            p.host_count[1] = 2u;
+            p.host_count[0] = 0u;
+        }
+        return;
+    }
     publish_search(p.counter, p.out, p.cap, p.host_count, p.dst, p.k_out, p.epi_cap, smem,
                    p.debug == 9);
     __syncthreads();

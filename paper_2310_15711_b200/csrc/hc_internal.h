@@ -36,7 +36,8 @@ struct KParams {
     uint32_t *out;       // positions (window starts), unordered; NULL = count only
     uint32_t cap;        // capacity of out
     uint32_t *counter;   // kCtr words: [0] = total occurrences (may exceed cap), [1] = staged
-                         // tile counter, [2] = CTAs done (epilogue ticket); zero between calls
+                         // tile counter, [2] = CTAs done (epilogue ticket), [3] = give-up
+                         // flag (gather); zero between calls
     // fused epilogue (the last CTA to finish): count publication + ordering
     uint32_t *host_count;  // mapped pinned [2]: count, then 1 if the positions were ordered
                            // into dst by the epilogue (else the host orders them)
@@ -44,6 +45,7 @@ struct KParams {
     uint32_t k_out;      // min(max_out, windows)
     uint32_t epi_cap;    // largest count the epilogue orders in its CTA's shared memory
     uint32_t nbits;      // positions are < 2^nbits
+    uint32_t allow_abort;  // gather path: may give up on walk-heavy text (host_count[1] = 2)
     uint32_t debug;      // 1: staged kernel skips the search (pipeline measurement only)
     uint32_t tma_chunk;  // staged: split each tile's bulk copy into pieces of this size (0 = one)
     unsigned long long *trace;  // staged: per-(CTA, tile) %globaltimer events (debugging), or NULL
@@ -84,6 +86,9 @@ int mstream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t 
                        uint32_t bufs);
 cudaError_t launch_gather(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li);
+cudaError_t launch_scan(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
+                        LaunchInfo *li);
+int scan_smem_bytes(uint32_t alpha, uint32_t m, uint32_t q, uint32_t buf_bytes);
 // Ordering of `count` distinct positions (u32, unordered) into dst: the smallest k,
 // ascending, as int64.  Used when the search kernel's epilogue did not order them
 // (count above its shared-memory capacity, or skewed).  count <= kSmallSort: one CTA

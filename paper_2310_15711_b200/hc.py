@@ -28,7 +28,7 @@ _lib = C.CDLL(LIB_PATH)
 
 HC_OK, HC_EINVAL, HC_ETOOSHORT, HC_EALPHA, HC_ENOMEM, HC_ECUDA, HC_ETOOLONG, HC_ENODEV = (
     0, -1, -2, -3, -4, -5, -6, -7)
-PATH_AUTO, PATH_STAGED, PATH_GATHER, PATH_STREAM, PATH_SHC = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_STAGED, PATH_GATHER, PATH_STREAM, PATH_SHC, PATH_SCAN = 0, 1, 2, 3, 4, 5
 WORD_BITS = 32
 
 # the symbols include/hc.h declares (tests check every one is exported)

@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
 from paper_2310_15711_b200 import hc  # noqa: E402
 from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
-PATHS = [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC, hc.PATH_AUTO]
+PATHS = [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC, hc.PATH_SCAN, hc.PATH_AUTO]
 
 
 def to_dev(y: np.ndarray, offset: int = 0):
@@ -80,7 +80,8 @@ def test_random_small(path):
         assert np.array_equal(got, want), (trial, m, q, alpha, n, off, len(want), len(got))
 
 
-@pytest.mark.parametrize("path", [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC])
+@pytest.mark.parametrize("path", [hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC,
+                                  hc.PATH_SCAN])
 @pytest.mark.parametrize("max_ctas,stages", [(1, 2), (2, 3), (3, 4), (5, 1)])
 def test_many_tiles_per_cta(path, max_ctas, stages):
     # tiny tiles / few CTAs: every CTA cycles its TMA ring many times
@@ -303,7 +304,7 @@ def test_search_batch_matches_single_searches():
     assert cnts == [len(w) for w in want]
 
 
-@pytest.mark.parametrize("path", [hc.PATH_STREAM, hc.PATH_GATHER, hc.PATH_SHC])
+@pytest.mark.parametrize("path", [hc.PATH_STREAM, hc.PATH_GATHER, hc.PATH_SHC, hc.PATH_SCAN])
 def test_ordering_paths(path):
     """Occurrence counts across every ordering branch of the finish kernel (rank count
     <= 256, bucket pass, skewed buckets -> block radix sort, > 8192 -> device sort),
@@ -394,7 +395,8 @@ def test_prepare_batch_equals_prepare():
         hc.prepare_batch([b"abc", b"a"], 2, 8)       # q > m for the second pattern
 
 
-@pytest.mark.parametrize("path", [hc.PATH_AUTO, hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC])
+@pytest.mark.parametrize("path", [hc.PATH_AUTO, hc.PATH_STAGED, hc.PATH_GATHER, hc.PATH_STREAM, hc.PATH_SHC,
+                                  hc.PATH_SCAN])
 def test_largest_tables_every_path(path):
     """alpha = 15 (F = 128 KiB, the largest table) with short and long patterns on every
     path: each either fits its shared-memory layout or falls back (stream -> gather);
@@ -409,7 +411,7 @@ def test_largest_tables_every_path(path):
         try:
             got = gpu(h, to_dev(y, 2), path=path)
         except hc.HCError as e:
-            assert path == hc.PATH_SHC and e.code == -1, (m, q, e)
+            assert path in (hc.PATH_SHC, hc.PATH_SCAN) and e.code == -1, (m, q, e)
             continue
         assert np.array_equal(got, want), (m, q)
 
@@ -456,7 +458,7 @@ def test_every_kernel_build(path):
                 try:
                     got = gpu(h, to_dev(yy, off), path=path)
                 except hc.HCError as e:        # SHC may refuse a layout it cannot fit
-                    assert path == hc.PATH_SHC and e.code == hc.HC_EINVAL, (q, alpha, m, e)
+                    assert path in (hc.PATH_SHC, hc.PATH_SCAN) and e.code == hc.HC_EINVAL, (q, alpha, m, e)
                     continue
                 assert np.array_equal(got, want), (q, s, alpha, m, off, len(got), len(want))
                 seen.add((q, s))
@@ -482,7 +484,7 @@ def test_long_patterns(path):
         try:
             got = gpu(h, to_dev(yy, 7), path=path)
         except hc.HCError as e:
-            assert path in (hc.PATH_SHC, hc.PATH_STAGED) and e.code == hc.HC_EINVAL, (m, e)
+            assert path in (hc.PATH_SHC, hc.PATH_STAGED, hc.PATH_SCAN) and e.code == hc.HC_EINVAL, (m, e)
             continue
         assert np.array_equal(got, want), (m, q, alpha, len(got), len(want))
     with pytest.raises(hc.HCError) as ei:

@@ -14,7 +14,7 @@ from paper_2310_15711_b200 import inputs as I  # noqa: E402
 
 cfg = I.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 ms = [int(a) for a in sys.argv[2:]] or list(cfg.ms)
-y_np, _ = I.config_text(cfg)
+y_np, block = I.config_text(cfg)
 y = torch.from_numpy(y_np).cuda()
 n = len(y_np)
 flush = torch.ones(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8, device="cuda")
@@ -23,7 +23,7 @@ pos = torch.empty(1 << 24, dtype=torch.int64, device="cuda")
 st = hc.Stats()
 for m in ms:
     q, a = cfg.qa[m]
-    hs = [hc.prepare(x, q, a) for _, x in I.patterns(cfg, y_np, m)[:4]]
+    hs = [hc.prepare(x, q, a) for _, x in I.patterns(cfg, y_np, m, block=block)[:4]]
     t = {"pos": [], "count": []}
     for r in range(4):
         for h in hs:
