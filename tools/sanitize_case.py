@@ -49,7 +49,7 @@ def main():
     ya = np.full(n, ord("A"), np.uint8)
     cases.append((np.frombuffer(b"AAAA", np.uint8).copy(), 2, 10, ya))
     bad = 0
-    paths = [hc.PATH_STREAM, hc.PATH_GATHER, hc.PATH_STAGED, hc.PATH_SHC]
+    paths = [hc.PATH_STREAM, hc.PATH_GATHER, hc.PATH_STAGED, hc.PATH_SHC, hc.PATH_SCAN]
     for x, q, a, yy in cases:
         want = oracle.brute(x, yy)
         yd = torch.from_numpy(yy).cuda()
@@ -58,7 +58,7 @@ def main():
             try:
                 got = hc.search(h, yd, path=path, debug=dbg).cpu().numpy()
             except hc.HCError as e:
-                if e.code == hc.HC_EINVAL and path in (hc.PATH_SHC, hc.PATH_STAGED):
+                if e.code == hc.HC_EINVAL and path in (hc.PATH_SHC, hc.PATH_STAGED, hc.PATH_SCAN):
                     continue
                 raise
             if not np.array_equal(got, want):
