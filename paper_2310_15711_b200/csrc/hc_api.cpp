@@ -293,7 +293,11 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         path = S <= kStagedMaxShift ? HC_PATH_STREAM : HC_PATH_GATHER;
         // the gather search may give up on walk-heavy text and be re-run on the scan path
         // (hc_gather.cu), when the scan path can take this pattern
+#ifdef HC_NO_ABORT
+        p.allow_abort = 0 &&
+#else
         p.allow_abort = path == HC_PATH_GATHER &&
+#endif
                         hc::scan_smem_bytes(p.alpha, m, q, 0) <= smem_budget(h->device);
     }
     if (path == HC_PATH_STAGED) {

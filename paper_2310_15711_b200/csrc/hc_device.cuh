@@ -47,6 +47,7 @@ namespace hc {
 constexpr uint32_t kWordBits = 32;       // w (R2)
 constexpr uint32_t kLongWalk = 4;        // walks past this many links with as many left go warp-wide
 constexpr uint32_t kCoopVerifyMin = 64;  // m above which verification is warp-wide
+constexpr uint32_t kAbortWalks = 16;     // warp-wide walks in one phase-B batch: walk-heavy text
 constexpr int kUnroll = 4;               // lattice rounds whose loads are issued together
 constexpr int kWalkUnroll = 4;           // walk steps evaluated per phase-B iteration
 constexpr uint32_t kSurvWarps = 2;       // staged: survivor/producer warps per CTA
@@ -444,6 +445,14 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
     bool walk = false;
     const bool long_walks = p.m >= 2 * kLongWalk * Q;   // warp-wide walks can pay off
     if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 5, 1u);
+    // Walk-heavy text (allow_abort, gather path): Fig. 5's loop would re-hash most q-grams
+    // many times over (the stress config C5: ~7 hashes per text byte).  A batch that needs
+    // more than kAbortWalks warp-wide walks raises the give-up flag, and every later
+    // batch returns as soon as it would start a warp-wide walk: the search finishes its
+    // (cheap) lattice filter and first steps, and the host re-runs it on the scan path,
+    // which hashes every q-gram once (hc_scan.cu).  Only batches with warp-wide walks (rare
+    // on non-repetitive text) read the flag.
+    uint32_t nwalks = 0;
     while (__any_sync(HC_FULL, active)) {
         if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 4, 1u);
         bool need_v = false, stepped = false;
@@ -452,6 +461,14 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
             // go (near-matches, true matches) finish warp-wide, one lane at a time
             uint32_t lm = __ballot_sync(HC_FULL, active && walk && wsteps >= kLongWalk &&
                                                      (j - i) >= kLongWalk * Q);
+            if (p.allow_abort && lm) {
+                volatile uint32_t *flag = p.counter + 3;
+                if (nwalks == 0 && *flag) return wo.cnt;     // another batch gave up already
+                if ((nwalks += __popc(lm)) > kAbortWalks) {
+                    if (lane == 0) *flag = 1u;
+                    return wo.cnt;
+                }
+            }
             while (lm) {
                 const uint32_t L = __ffs(lm) - 1;
                 lm &= lm - 1;
@@ -657,13 +674,6 @@ __device__ __forceinline__ bool first_steps_eval(const KParams &p, const T &txt,
 // time through first_steps_eval; the segments that continue go to a second queue
 // (q2, window ends) that runs phase B whenever 32 are queued (both queues may span
 // chunks, since the survivors read global memory).
-// Walk-heavy text (KParams::allow_abort, gather path): when more than half of a warp's
-// first lattice survivors walk on past their first link test, Fig. 5's loop would
-// re-hash most q-grams many times over (the stress config C5: ~7 hashes per text byte);
-// the warp raises the give-up flag before any walk runs, every warp stops at its next
-// chunk, and the host re-runs the search on the scan path, which hashes every q-gram
-// once (hc_scan.cu).
-constexpr uint32_t kAbortMinSurvivors = 32;
 template <int Q, int SH, class T, class FT = FTable>
 struct WarpQueueSink {
     const KParams &p;
@@ -675,9 +685,6 @@ struct WarpQueueSink {
     WarpOut &wo;
     uint32_t lane;
     uint32_t pi = 0;       // pattern index (launch parameters s_params[pi])
-    uint32_t n_surv = 0;   // lattice survivors through first steps (warp-uniform)
-    uint32_t n_walk = 0;   // ... of which the walk went on past its first link test
-    bool gave_up = false;  // allow_abort: walk-heavy text detected (see hc_gather.cu)
     __device__ __forceinline__ void steps(uint32_t c) {  // first steps of q1[0..c) -> q2
         const bool act = lane < c;
         steps_e(act, act ? q1[lane] : 0u);
@@ -690,15 +697,6 @@ struct WarpQueueSink {
         uint32_t start;
         const bool keep = first_steps_eval<Q, SH>(p, t2, sF, act, e, start);
         const uint32_t bm = __ballot_sync(HC_FULL, keep);
-        n_surv += __popc(__ballot_sync(HC_FULL, act));
-        n_walk += __popc(__ballot_sync(HC_FULL, keep && start == e));
-        if (p.allow_abort && n_surv >= kAbortMinSurvivors && 2 * n_walk > n_surv) {
-            // walk-heavy text: give up before the walks (phase B) cost anything
-            if (lane == 0) *reinterpret_cast<volatile uint32_t *>(p.counter + 3) = 1u;
-            gave_up = true;
-            n1 = n2 = 0;
-            return;
-        }
         if (keep) q2[n2 + __popc(bm & lanemask_lt())] = start;
         n2 += __popc(bm);
         if (n2 >= 32) {
@@ -713,7 +711,6 @@ struct WarpQueueSink {
         }
     }
     __device__ __forceinline__ void operator()(uint32_t bm, bool pass, uint32_t e) {
-        if (gave_up) return;
         if (pass) q1[n1 + __popc(bm & lanemask_lt())] = e;
         n1 += __popc(bm);
         if (n1 >= 32) {
@@ -1056,9 +1053,13 @@ __device__ __forceinline__ void publish_search(uint32_t *counter, const uint32_t
 }
 
 // Largest count the epilogue orders in `smem_bytes` of dynamic shared memory.
+#ifndef HC_EPI_MAX
+#define HC_EPI_MAX 8192
+#endif
 inline uint32_t epi_cap_for(int smem_bytes) {
     uint32_t c = smem_bytes > 544 ? (static_cast<uint32_t>(smem_bytes) - 544u) / 12u : 0u;
-    return c < kSmallSort ? c : kSmallSort;
+    c = c < kSmallSort ? c : kSmallSort;
+    return c < HC_EPI_MAX ? c : HC_EPI_MAX;
 }
 
 // Single-pattern kernels: the epilogue of search p (call from every thread at the end).

@@ -37,21 +37,13 @@ int gather_smem_bytes(uint32_t alpha, uint32_t m) {
 // chunk's loads are issued before this chunk's survivors are handed to the sink
 // (first steps / phase B round trips), so they overlap.  The first chunk's loads are
 // issued before the table load (`W` comes in loaded).
-// Walk-heavy text (allow_abort, WarpQueueSink): the give-up flag is read with the next
-// chunk's loads, so a normal search pays no extra round trip.
 template <int Q, int SH, int L, class Sink>
 __device__ __forceinline__ void gather_loop(const KParams &p, const GlobalText &txt, const FBits &fb,
                                             uint32_t c, uint32_t total_warps, uint32_t lane,
                                             uint64_t (&W)[4], Sink &sink, uint64_t *bar,
                                             bool &ready) {
     const uint32_t step = 32 * p.S;
-    volatile uint32_t *flag = p.counter + 3;
-    uint32_t give_up = 0;
     while (c < p.nchunks) {
-        if (p.allow_abort) {
-            if (__shfl_sync(HC_FULL, give_up, 0)) return;
-            if (lane == 0) give_up = *flag;           // consumed at the next chunk
-        }
         const uint32_t k0 = c * 32 * L;
         const uint32_t pos0 = p.m - 1 + (k0 + lane) * p.S;
         bool pass[L];
@@ -78,7 +70,6 @@ __device__ __forceinline__ void gather_loop(const KParams &p, const GlobalText &
                 const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
                 if (bm) sink(bm, pass[u], pos0 + u * step);
             }
-            if (sink.gave_up) return;
         }
     }
 }
@@ -142,7 +133,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
         gather_loop<Q, SH, 1>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
     if (!ready) mbar_wait(bar, 0);
     if (kInstrument && lane == 0) trace_event(p, warp, 1);          // lattice filtered
-    if (!(p.allow_abort && *reinterpret_cast<volatile uint32_t *>(p.counter + 3))) sink.drain();
+    sink.drain();
     if (kInstrument && lane == 0) trace_event(p, warp, 2);          // survivors done
     wo.flush(p, lane);
     if (kInstrument && lane == 0) trace_event(p, warp, 3);          // flushed

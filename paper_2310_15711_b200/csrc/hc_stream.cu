@@ -216,7 +216,12 @@ __device__ __forceinline__ void stream_loop_tma(const KParams &p, const FTable &
 }
 
 template <int Q, int SH>
-__global__ void __launch_bounds__(kStreamMaxThreads) stream_kernel(const KParams p) {
+#ifndef HC_STREAM_MINB
+#define HC_STREAM_MINB 3
+#endif
+// 3 CTAs per SM at most (shared memory allows 2-3): up to 85 registers, no spills in the
+// filter loop (at 64 the loop spilled ~600 B per thread)
+__global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t NW = blockDim.x / 32;
     const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages);

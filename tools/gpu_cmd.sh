@@ -1,3 +1,2 @@
-python -m pytest tests -m gpu -x -q -k "not slow" > gpurun_out/tq.log 2>&1; echo rc=$? >> gpurun_out/tq.log
-python tools/profile_search.py --config C5 --m 32 256 --reps 2 --path 5 > gpurun_out/c5scan.log 2>&1
-python tools/profile_search.py --config C2 --m 8 32 256 --reps 2 --path 5 > gpurun_out/c2scan.log 2>&1
+python tools/ab.py paper_2310_15711_b200/libhc_base.so paper_2310_15711_b200/libhc_noab.so --m 64 128 256 512 1024 --per-m 3 --reps 4 > gpurun_out/ab_noab.log 2>&1
+python tools/ab.py paper_2310_15711_b200/libhc_noab.so paper_2310_15711_b200/libhc.so --m 64 128 256 512 1024 --per-m 3 --reps 4 > gpurun_out/ab_noab2.log 2>&1
