@@ -11,9 +11,11 @@ of the config once with a single hc_search call (the north star's call: search
 kernel, count read-back, ordering of the positions into the caller's int64
 buffer), i.e. 800 searches of 256 MiB.  L2 is flushed (2 x L2 bytes read) before
 every call, outside the timed intervals; each call's device time comes from CUDA
-events the library records on the caller's stream (time_kernel = 2: from the
-search launch to the end of the call's last kernel, and the search kernel alone
-for the roofline).  value = bytes searched / summed device time.
+events the library records on the caller's stream around the call's device work
+(time_kernel = 1).  An hc_search is one kernel launch (search + fused epilogue)
+unless it re-runs or needs a host-launched ordering, so for single-launch calls
+that time is the search kernel's own duration (the roofline).  value = bytes
+searched / summed device time.
 
 Reported beside it (never in `value`): the same patterns through hc_search_batch
 (one call per m; multi-pattern launches), per-m single-call numbers on C3 and C4,
@@ -293,7 +295,10 @@ def main():
     counts = [hc.search_raw(h, y.data_ptr(), n, None, 0, sp) for h in handles]
     cap = max(1, max(counts))
     pos = torch.empty(cap, dtype=torch.int64, device=dev)
-    opts = hc.Opts(path=0, time_kernel=2)
+    # time_kernel = 1: CUDA events on the caller's stream around the call's device work.
+    # hc_search is ONE kernel launch (search + fused epilogue) unless a re-run or a host
+    # ordering is needed, so for single-launch calls this IS the search kernel's duration.
+    opts = hc.Opts(path=0, time_kernel=1)
     st = hc.Stats()
     if shard_mode:
         from paper_2310_15711_b200.shard import shard_bounds, gather_positions
@@ -322,7 +327,9 @@ def main():
                 c = hc.search_raw(h, y.data_ptr(), n, pos.data_ptr(), cap, sp, opts, st)
                 assert c == counts[k]
             launches += st.launches
-            per.append((st.kernel_ms, st.search_ms, st.path, st.reruns))
+            # the search kernel's own duration: the whole call when it was one launch
+            per.append((st.kernel_ms, st.kernel_ms if st.launches == 1 else float("nan"), st.path,
+                        st.reruns))
         torch.cuda.synchronize(dev)
         times = [p[0] for p in per]
         if shard_mode:
@@ -377,7 +384,8 @@ def main():
             bm.setdefault(m, []).append(k)
         for m, ks in bm.items():
             t = [times_per_step[s][k] for s in range(len(times_per_step)) for k in ks]
-            sk = [per_per_step[s][k][1] for s in range(len(per_per_step)) for k in ks]
+            sk = [per_per_step[s][k][1] for s in range(len(per_per_step)) for k in ks
+                  if per_per_step[s][k][1] == per_per_step[s][k][1]]
             med = statistics.median(t)
             agg = n_ * len(t) / (sum(t) / 1e3) / 1e9
             q, a = work_[ks[0]][1], work_[ks[0]][2]
@@ -387,7 +395,7 @@ def main():
                 "GBps_min": round(n_ / (max(t) / 1e3) / 1e9, 1),
                 "GBps_max": round(n_ / (min(t) / 1e3) / 1e9, 1),
                 "device_us_median": round(med * 1e3, 2),
-                "search_kernel_us_median": round(statistics.median(sk) * 1e3, 2),
+                "search_kernel_us_median": round(statistics.median(sk) * 1e3, 2) if sk else None,
                 "pct_of_measured_hbm": round(100 * n_ / (med / 1e3) / 1e9 / peak, 1),
                 "pct_of_8TBps": round(100 * n_ / (med / 1e3) / 1e9 / 8000, 1),
                 "meets_4000GBps": bool(n_ / (med / 1e3) / 1e9 >= TARGET_GBPS),
@@ -414,6 +422,8 @@ def main():
     for s in range(args.steps):
         for k, (m, q, a, o, x) in enumerate(work):
             kms, sms, path, _ = all_per[s][k]
+            if sms != sms:          # not a single launch (re-run or host ordering)
+                continue
             pn = PATH_NAMES.get(path, "?")
             shares[pn] = shares.get(pn, 0.0) + sms
             alg[pn] = alg.get(pn, 0.0) + F32.get(m, 1.0) * n + 4 * counts[k]
@@ -435,7 +445,9 @@ def main():
                                        "frac": round(alg[p_] / kt[p_] / 1e9 / peak, 4)}
                                   for p_ in shares if p_ != dom and kt[p_] > 0},
                 "algorithmic_bytes": "f(m) * n per launch (SURVEY 8(d) sector fractions; f = 1 "
-                                     "for m <= 32) + 4 B per position"}
+                                     "for m <= 32) + 4 B per position",
+                "duration": "CUDA events around each single-launch hc_search call of the timed "
+                            "region (the launch IS the search kernel with its fused epilogue)"}
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
@@ -451,8 +463,9 @@ def main():
                        "l2": "flushed (2 x L2 bytes read, clean eviction) before every call, "
                              "outside the timed intervals",
                        "timing": "sum over calls of the library's CUDA-event device time per "
-                                 "hc_search call on the caller's stream (search kernel, finish "
-                                 "kernel, re-runs and large ordering when they run)",
+                                 "hc_search call on the caller's stream (one search kernel with "
+                                 "its fused epilogue; re-runs and host-launched ordering when "
+                                 "they run)",
                        "wall_ms_per_step_incl_flush": round(1000 * t_wall / args.steps, 2),
                        "text_sha256": I.sha256(y_np)[:16]},
             "pct_of_measured_hbm": round(100 * value / peak, 1),
