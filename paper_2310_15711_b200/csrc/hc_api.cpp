@@ -733,9 +733,18 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
             continue;
         }
         const bool ordered = hcnt[1] != 0;
-        if (HC_INSTRUMENT && o.debug == 5 && stats) {
-            cudaMemcpy(stats->dbg, sc->buf + 4, 8, cudaMemcpyDeviceToHost);
-            cudaMemset(sc->buf + 4, 0, 8);
+#if HC_INSTRUMENT
+        if (o.debug == 10) {
+            unsigned long long ts[8] = {};
+            hc::read_epi_ts(ts);
+            std::fprintf(stderr, "epilogue block_order phases (ns): load %llu minmax %llu hist %llu "
+                                 "scan %llu scatter %llu rank %llu\n", ts[1] - ts[0], ts[2] - ts[1],
+                         ts[3] - ts[2], ts[4] - ts[3], ts[5] - ts[4], ts[6] - ts[5]);
+        }
+#endif
+        if (HC_INSTRUMENT && (o.debug == 5 || o.debug == 10) && stats) {
+            cudaMemcpy(stats->dbg, sc->buf + (o.debug == 5 ? 4 : 6), 8, cudaMemcpyDeviceToHost);
+            cudaMemset(sc->buf + 4, 0, 16);
         }
         if (want_pos && count > cap) {
             // position scratch overflowed: the count is exact, re-run with room for all

@@ -951,6 +951,12 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t *c, uint32_t N
 // minimum (power-of-two buckets, count/2 to count of them) and rank counting inside
 // each bucket.  Returns false when some bucket holds more than kEpiBucketMax keys
 // (strongly clustered positions): the host then orders them (nothing is assumed of dst).
+#if HC_INSTRUMENT
+static __device__ unsigned long long g_epi_ts[8];   // debug 10: block_order phase stamps
+#define HC_EPI_TS(i) do { if (threadIdx.x == 0) g_epi_ts[i] = gtimer(); } while (0)
+#else
+#define HC_EPI_TS(i) do { } while (0)
+#endif
 constexpr uint32_t kEpiRankMax = 256;
 constexpr uint32_t kEpiBucketMax = 64;
 static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t count, int64_t *dst, uint32_t k,
@@ -963,8 +969,10 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
     for (uint32_t i = 4 * t; i < count; i += 4 * T)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(ks + i)), "l"(pos + i)
                      : "memory");
+    HC_EPI_TS(0);
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    HC_EPI_TS(1);
     if (count <= kEpiRankMax) {
         for (uint32_t i = t; i < count; i += T) {
             const uint32_t key = ks[i];
@@ -990,17 +998,21 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
     // bucket = (key - lo) >> sh with (hi - lo) >> sh < NB
     uint32_t sh = 0;
     while (((hi - lo) >> sh) >= NB) ++sh;
+    HC_EPI_TS(2);
     for (uint32_t i = t; i < count; i += T) atomicAdd(&c[(ks[i] - lo) >> sh], 1u);
     __syncthreads();
+    HC_EPI_TS(3);
     uint32_t big = 0;
     for (uint32_t i = t; i < NB; i += T) big |= c[i] > kEpiBucketMax;
     if (__syncthreads_or(big)) return false;
     block_exclusive_scan(c, NB, tmp);                            // c[b] = start of bucket b
+    HC_EPI_TS(4);
     for (uint32_t i = t; i < count; i += T) {
         const uint32_t key = ks[i];
         k2[atomicAdd(&c[(key - lo) >> sh], 1u)] = key;           // c[b] ends at bucket b's end
     }
     __syncthreads();
+    HC_EPI_TS(5);
     for (uint32_t i = t; i < count; i += T) {
         const uint32_t key = k2[i];
         const uint32_t b = (key - lo) >> sh;
@@ -1009,6 +1021,8 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
         for (uint32_t j = b_lo; j < b_hi; ++j) r += k2[j] < key;
         if (r < k) dst[r] = static_cast<int64_t>(key);
     }
+    __syncthreads();
+    HC_EPI_TS(6);
     return true;
 }
 
@@ -1038,7 +1052,13 @@ __device__ __forceinline__ void publish_search(uint32_t *counter, const uint32_t
             if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(__ldcg(out));
             ordered = true;
         } else {
+            unsigned long long t0 = 0;
+            if (kInstrument && threadIdx.x == 0) t0 = gtimer();
             ordered = block_order(out, count, dst, k_out, smem);
+            if (kInstrument && threadIdx.x == 0) {   // debug 10: ordering time, ns
+                counter[6] = static_cast<uint32_t>(gtimer() - t0);
+                counter[7] = count;
+            }
         }
     }
     __syncthreads();

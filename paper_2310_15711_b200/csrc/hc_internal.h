@@ -97,6 +97,9 @@ int scan_smem_bytes(uint32_t alpha, uint32_t m, uint32_t q, uint32_t buf_bytes);
 cudaError_t order_positions(const uint32_t *pos, uint32_t count, uint32_t n, int64_t *dst,
                             uint32_t k, cudaStream_t st, int *launches);
 constexpr uint32_t kSmallSort = 8192;
+#if defined(HC_INSTRUMENT) && HC_INSTRUMENT
+cudaError_t read_epi_ts(unsigned long long *host8);   // hc_stream.cu, debug 10
+#endif
 inline uint32_t bits_for(uint32_t n) {   // positions < n fit in bits_for(n) bits
     uint32_t b = 1;
     while (b < 32 && (static_cast<uint64_t>(1) << b) < n) ++b;

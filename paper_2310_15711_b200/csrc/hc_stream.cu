@@ -264,6 +264,12 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
     search_epilogue(p, smem);
 }
 
+#if HC_INSTRUMENT
+cudaError_t read_epi_ts(unsigned long long *host8) {   // debug 10 (this TU's stamps)
+    return cudaMemcpyFromSymbol(host8, g_epi_ts, sizeof(unsigned long long) * 8);
+}
+#endif
+
 template <int Q, int SH>
 struct PickStream {
     using Fn = KernFn;

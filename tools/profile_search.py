@@ -96,7 +96,9 @@ def main():
             torch.cuda.synchronize()
             print(f"m={m} q={q} a={a} rep={r} count={len(res)} kernel_us={st['kernel_ms']*1e3:.1f} "
                   f"GBps={len(y)/(st['kernel_ms']/1e3)/1e9:.0f} grid={st['grid']} smem={st['smem_bytes']}"
-                  + (f" phaseB iters={st['dbg'][0]} calls={st['dbg'][1]}" if args.debug == 5 else ""),
+                  + (f" phaseB iters={st['dbg'][0]} calls={st['dbg'][1]}" if args.debug == 5 else "")
+                  + (f" epilogue ordering {st['dbg'][0] / 1e3:.2f} us for {st['dbg'][1]} positions"
+                     if args.debug == 10 else ""),
                   flush=True)
             if args.trace and r == args.reps - 1 and st["path"] == 2:
                 # gather: per-warp events (trace_tiles >= 8): table loaded, filtered, drained, flushed
