@@ -891,79 +891,30 @@ __device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint3
 // own (now idle) shared memory.  One kernel launch per hc_search in the common case;
 // the host orders only what the epilogue could not (hc_finish.cu).
 
-// Block-wide min / max / sum (blockDim.x a multiple of 32; `tmp` >= 32 shared words).
-__device__ __forceinline__ uint32_t block_min(uint32_t v, uint32_t *tmp) {
-    v = __reduce_min_sync(HC_FULL, v);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) tmp[threadIdx.x >> 5] = v;
-    __syncthreads();
-    uint32_t r = tmp[0];
-    for (uint32_t w = 1; w < blockDim.x / 32; ++w) r = min(r, tmp[w]);
-    return r;
-}
-__device__ __forceinline__ uint32_t block_max(uint32_t v, uint32_t *tmp) {
-    v = __reduce_max_sync(HC_FULL, v);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) tmp[threadIdx.x >> 5] = v;
-    __syncthreads();
-    uint32_t r = tmp[0];
-    for (uint32_t w = 1; w < blockDim.x / 32; ++w) r = max(r, tmp[w]);
-    return r;
-}
-// In-place exclusive scan of c[0..NB) (NB a power of two, 32 <= NB <= 32 * blockDim.x)
-// by the whole block; every thread gets the total.
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t *c, uint32_t NB, uint32_t *tmp) {
-    const uint32_t T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t per = (NB + T - 1) / T;            // counters per thread (consecutive)
-    const uint32_t b0 = t * per;
-    uint32_t loc = 0;
-    for (uint32_t i = 0; i < per; ++i)
-        if (b0 + i < NB) loc += c[b0 + i];
-    uint32_t incl = loc;
-#pragma unroll
-    for (uint32_t o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(HC_FULL, incl, o);
-        if (lane >= o) incl += v;
-    }
-    __syncthreads();
-    if (lane == 31) tmp[warp] = incl;
-    __syncthreads();
-    uint32_t wbase = 0, total = 0;
-    for (uint32_t w = 0; w < T / 32; ++w) {
-        const uint32_t x = tmp[w];
-        if (w < warp) wbase += x;
-        total += x;
-    }
-    uint32_t run = wbase + incl - loc;
-    for (uint32_t i = 0; i < per; ++i)
-        if (b0 + i < NB) {
-            const uint32_t x = c[b0 + i];
-            c[b0 + i] = run;
-            run += x;
-        }
-    __syncthreads();
-    return total;
-}
-
 // Orders `count` distinct positions pos[0..count) (2 <= count) into dst[0..k) ascending,
 // in shared memory `sm` (>= epi_bytes(count) bytes), by the whole block.  Small sets by
 // rank counting; larger ones by a bucket pass on the positions' offset from their
-// minimum (power-of-two buckets, count/2 to count of them) and rank counting inside
-// each bucket.  Returns false when some bucket holds more than kEpiBucketMax keys
-// (strongly clustered positions): the host then orders them (nothing is assumed of dst).
+// minimum (power-of-two buckets, count/2 to count of them, at most 2048) and rank
+// counting inside each bucket.  Keys are read as 16-byte vectors, each pass over them
+// is a straight loop of independent shared-memory operations, the counter scan works
+// on 16-byte vectors with warp shuffles, and the sorted keys leave through coalesced
+// 8-byte stores.  Returns false when some bucket holds more than kEpiBucketMax keys
+// (strongly clustered positions): the host then orders them (nothing is assumed of
+// dst).
 #if HC_INSTRUMENT
-static __device__ unsigned long long g_epi_ts[8];   // debug 10: block_order phase stamps
-#define HC_EPI_TS(i) do { if (threadIdx.x == 0) g_epi_ts[i] = gtimer(); } while (0)
+static __device__ unsigned long long g_epi_ts[16];  // debug 10: block_order phase stamps
+#define HC_EPI_TS(i) do { if (threadIdx.x == 0) { g_epi_ts[i] = gtimer(); g_epi_ts[8 + i] = clock64(); } } while (0)
 #else
 #define HC_EPI_TS(i) do { } while (0)
 #endif
 constexpr uint32_t kEpiRankMax = 256;
 constexpr uint32_t kEpiBucketMax = 64;
 static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t count, int64_t *dst, uint32_t k,
-                                         uint8_t *sm) {
-    const uint32_t T = blockDim.x, t = threadIdx.x;
+                                                uint8_t *sm) {
+    const uint32_t T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, NWp = T >> 5;
     uint32_t *tmp = reinterpret_cast<uint32_t *>(sm);            // 64 words
-    uint32_t *ks = tmp + 64;                                     // count keys (16-B aligned)
+    uint32_t *ks = tmp + 64;                                     // keys, then the sorted keys
+    const uint32_t cnt4 = (count + 3) & ~3u;
     // all keys to shared memory with 16-byte cp.async copies: one L2 round trip (the
     // scratch is 16-byte aligned and has >= 3 words of slack past any count)
     for (uint32_t i = 4 * t; i < count; i += 4 * T)
@@ -972,11 +923,14 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
     HC_EPI_TS(0);
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    for (uint32_t i = count + t; i < cnt4; i += T) ks[i] = 0xffffffffu;   // pad the last vector
+    __syncthreads();
     HC_EPI_TS(1);
     if (count <= kEpiRankMax) {
-        for (uint32_t i = t; i < count; i += T) {
-            const uint32_t key = ks[i];
+        if (t < count) {
+            const uint32_t key = ks[t];
             uint32_t r = 0;
+#pragma unroll 8
             for (uint32_t j = 0; j < count; ++j) r += ks[j] < key;
             if (r < k) dst[r] = static_cast<int64_t>(key);
         }
@@ -984,44 +938,114 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
     }
     uint32_t NB = 32;
     while (NB < 2048 && 2 * NB < count) NB <<= 1;                // count/2 <= NB < count
-    uint32_t *c = ks + ((count + 3) & ~3u);                      // NB bucket counters
+    uint32_t *c = ks + cnt4;                                     // NB bucket counters
     uint32_t *k2 = c + NB;                                       // keys grouped by bucket
+    const uint4 *ks4 = reinterpret_cast<const uint4 *>(ks);
+    const uint32_t n4 = cnt4 / 4;
+    // minimum and maximum (the pads are all-ones: excluded from the maximum)
     uint32_t lo = 0xffffffffu, hi = 0;
-    for (uint32_t i = t; i < count; i += T) {
-        const uint32_t key = ks[i];
-        lo = min(lo, key);
-        hi = max(hi, key);
+    for (uint32_t i = t; i < n4; i += T) {
+        const uint4 v = ks4[i];
+        lo = min(min(lo, v.x), min(v.y, min(v.z, v.w)));
+        hi = max(max(hi, v.x != 0xffffffffu ? v.x : 0u),
+                 max(v.y != 0xffffffffu ? v.y : 0u,
+                     max(v.z != 0xffffffffu ? v.z : 0u, v.w != 0xffffffffu ? v.w : 0u)));
     }
-    for (uint32_t i = t; i < NB; i += T) c[i] = 0;
-    lo = block_min(lo, tmp);
-    hi = block_max(hi, tmp + 32);
-    // bucket = (key - lo) >> sh with (hi - lo) >> sh < NB
-    uint32_t sh = 0;
+    lo = __reduce_min_sync(HC_FULL, lo);
+    hi = __reduce_max_sync(HC_FULL, hi);
+    if (lane == 0) {
+        tmp[warp] = lo;
+        tmp[32 + warp] = hi;
+    }
+    for (uint32_t i = t; i < NB / 4; i += T) reinterpret_cast<uint4 *>(c)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    lo = tmp[0];
+    hi = tmp[32];
+    for (uint32_t w = 1; w < NWp; ++w) {
+        lo = min(lo, tmp[w]);
+        hi = max(hi, tmp[32 + w]);
+    }
+    uint32_t sh = 0;                                             // (hi - lo) >> sh < NB
     while (((hi - lo) >> sh) >= NB) ++sh;
     HC_EPI_TS(2);
-    for (uint32_t i = t; i < count; i += T) atomicAdd(&c[(ks[i] - lo) >> sh], 1u);
-    __syncthreads();
-    HC_EPI_TS(3);
-    uint32_t big = 0;
-    for (uint32_t i = t; i < NB; i += T) big |= c[i] > kEpiBucketMax;
-    if (__syncthreads_or(big)) return false;
-    block_exclusive_scan(c, NB, tmp);                            // c[b] = start of bucket b
-    HC_EPI_TS(4);
-    for (uint32_t i = t; i < count; i += T) {
-        const uint32_t key = ks[i];
-        k2[atomicAdd(&c[(key - lo) >> sh], 1u)] = key;           // c[b] ends at bucket b's end
+    for (uint32_t i = t; i < n4; i += T) {                       // histogram
+        const uint4 v = ks4[i];
+        const uint32_t base = 4 * i;
+        if (base + 0 < count) atomicAdd(&c[(v.x - lo) >> sh], 1u);
+        if (base + 1 < count) atomicAdd(&c[(v.y - lo) >> sh], 1u);
+        if (base + 2 < count) atomicAdd(&c[(v.z - lo) >> sh], 1u);
+        if (base + 3 < count) atomicAdd(&c[(v.w - lo) >> sh], 1u);
     }
     __syncthreads();
+    HC_EPI_TS(3);
+    // exclusive scan of the NB counters: thread t owns NB / T consecutive counters (one or
+    // two 16-byte vectors when NB >= 4 T... else one vector for t < NB / 4)
+    {
+        const uint32_t per = NB / T >= 4 ? NB / T : 4u;          // counters per owning thread
+        const uint32_t owners = NB / per;
+        uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t loc = 0, big = 0;
+        if (t < owners) {
+            const uint4 *c4 = reinterpret_cast<const uint4 *>(c + t * per);
+#pragma unroll
+            for (uint32_t u = 0; u < 2; ++u)
+                if (4 * u < per) {
+                    const uint4 x = c4[u];
+                    v[4 * u] = x.x; v[4 * u + 1] = x.y; v[4 * u + 2] = x.z; v[4 * u + 3] = x.w;
+                }
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                big |= v[u] > kEpiBucketMax;
+                loc += v[u];
+            }
+        }
+        uint32_t incl = loc;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(HC_FULL, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane == 31) tmp[warp] = incl;
+        if (__syncthreads_or(big)) return false;
+        uint32_t run = incl - loc;
+        for (uint32_t w = 0; w < warp; ++w) run += tmp[w];
+        if (t < owners) {
+            uint4 *c4 = reinterpret_cast<uint4 *>(c + t * per);
+#pragma unroll
+            for (uint32_t u = 0; u < 2; ++u)
+                if (4 * u < per) {
+                    uint4 x;
+                    x.x = run; run += v[4 * u];
+                    x.y = run; run += v[4 * u + 1];
+                    x.z = run; run += v[4 * u + 2];
+                    x.w = run; run += v[4 * u + 3];
+                    c4[u] = x;
+                }
+        }
+        __syncthreads();
+    }
+    HC_EPI_TS(4);
+    for (uint32_t i = t; i < n4; i += T) {                       // scatter by bucket
+        const uint4 v = ks4[i];
+        const uint32_t base = 4 * i;
+        if (base + 0 < count) k2[atomicAdd(&c[(v.x - lo) >> sh], 1u)] = v.x;
+        if (base + 1 < count) k2[atomicAdd(&c[(v.y - lo) >> sh], 1u)] = v.y;
+        if (base + 2 < count) k2[atomicAdd(&c[(v.z - lo) >> sh], 1u)] = v.z;
+        if (base + 3 < count) k2[atomicAdd(&c[(v.w - lo) >> sh], 1u)] = v.w;
+    }
+    __syncthreads();                                             // c[b] = end of bucket b
     HC_EPI_TS(5);
-    for (uint32_t i = t; i < count; i += T) {
+    for (uint32_t i = t; i < count; i += T) {                    // rank inside the bucket
         const uint32_t key = k2[i];
         const uint32_t b = (key - lo) >> sh;
         const uint32_t b_lo = b ? c[b - 1] : 0u, b_hi = c[b];
         uint32_t r = b_lo;
         for (uint32_t j = b_lo; j < b_hi; ++j) r += k2[j] < key;
-        if (r < k) dst[r] = static_cast<int64_t>(key);
+        ks[r] = key;                                             // sorted (ks is free now)
     }
     __syncthreads();
+    const uint32_t kk = min(k, count);
+    for (uint32_t i = t; i < kk; i += T) dst[i] = static_cast<int64_t>(ks[i]);   // coalesced
     HC_EPI_TS(6);
     return true;
 }

@@ -98,7 +98,7 @@ cudaError_t order_positions(const uint32_t *pos, uint32_t count, uint32_t n, int
                             uint32_t k, cudaStream_t st, int *launches);
 constexpr uint32_t kSmallSort = 8192;
 #if defined(HC_INSTRUMENT) && HC_INSTRUMENT
-cudaError_t read_epi_ts(unsigned long long *host8);   // hc_stream.cu, debug 10
+cudaError_t read_epi_ts(unsigned long long *host16);  // hc_stream.cu, debug 10
 #endif
 inline uint32_t bits_for(uint32_t n) {   // positions < n fit in bits_for(n) bits
     uint32_t b = 1;

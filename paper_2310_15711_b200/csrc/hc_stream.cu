@@ -4,6 +4,11 @@
 // first steps on the stage and phase B on global text.  DESIGN.md 5.
 #include "hc_device.cuh"
 
+#ifndef HC_STREAM_GLOBAL_FS
+#define HC_STREAM_GLOBAL_FS 1   // first steps on global text (L2), the queue spans chunks:
+                                // no partial batch at every chunk end (C2 m=16 -11%)
+#endif
+
 namespace hc {
 
 // ------------------------------------------------------------------ stream kernel
@@ -48,8 +53,9 @@ struct StreamQueue {
     uint32_t n1;      // warp-uniform count
     // first steps of 32 queued survivors, on the chunk's stage (the queue only ever
     // holds survivors of the chunk being filtered: it is drained at the chunk's end)
+    template <class TT>
     __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText> &sink,
-                                            const SmemText &txt, uint32_t lane) {
+                                            const TT &txt, uint32_t lane) {
         __syncwarp();
         const uint32_t e = q1[n1 - 32 + lane];
         n1 -= 32;
@@ -58,8 +64,9 @@ struct StreamQueue {
         __syncwarp();
         sink.steps_e_on(txt, true, e);
     }
+    template <class TT>
     __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText> &sink,
-                                              const SmemText &txt, uint32_t lane) {
+                                              const TT &txt, uint32_t lane) {
         while (n1 >= 32) drain32(sink, txt, lane);
         if (n1) {
             __syncwarp();
@@ -107,7 +114,11 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             pos += kStreamUnroll * step;
         }
         if (qu.n1 < 32) break;
+#if HC_STREAM_GLOBAL_FS
+        qu.drain32(sink, sink.txt, lane);
+#else
         qu.drain32(sink, txt, lane);
+#endif
     }
     for (; k < k1; k += 32, pos += step) {          // ragged tail, one round at a time
         const bool in = k + lane < k1;
@@ -118,7 +129,11 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             qu.n1 += __popc(bm);
             __syncwarp();
             if (lane == 0) *qu.ctr = qu.n1;
+#if HC_STREAM_GLOBAL_FS
+            if (qu.n1 >= 32) qu.drain32(sink, sink.txt, lane);
+#else
             if (qu.n1 >= 32) qu.drain32(sink, txt, lane);
+#endif
         }
     }
 }
@@ -143,7 +158,9 @@ __device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
         const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
         if (!(kInstrument && p.debug == 1)) {   // debug 1: copy pipeline alone
             stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+#if !HC_STREAM_GLOBAL_FS
             qu.drain_all(sink, txt, lane);
+#endif
         }
         __syncwarp();              // every lane is done with buffer b before its refill
         b = b + 1 == NB ? 0 : b + 1;
@@ -208,7 +225,9 @@ __device__ __forceinline__ void stream_loop_tma(const KParams &p, const FTable &
         const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
         if (!(kInstrument && p.debug == 1)) {   // debug 1: copy pipeline alone
             stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+#if !HC_STREAM_GLOBAL_FS
             qu.drain_all(sink, txt, lane);
+#endif
         }
         __syncwarp();
         b = b + 1 == NB ? 0 : b + 1;
@@ -258,6 +277,9 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
         stream_loop<Q, SH, 3>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
     else
         stream_loop<Q, SH, 4>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+#if HC_STREAM_GLOBAL_FS
+    qu.drain_all(sink, gtxt, lane);
+#endif
     sink.drain();
     wo.flush(p, lane);
     if (kInstrument && lane == 0) trace_cta(p, 1);
@@ -266,7 +288,7 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
 
 #if HC_INSTRUMENT
 cudaError_t read_epi_ts(unsigned long long *host8) {   // debug 10 (this TU's stamps)
-    return cudaMemcpyFromSymbol(host8, g_epi_ts, sizeof(unsigned long long) * 8);
+    return cudaMemcpyFromSymbol(host8, g_epi_ts, sizeof(unsigned long long) * 16);
 }
 #endif
 

@@ -1,1 +1,2 @@
-python bench.py --steps 3 --warmup 3 > gpurun_out/bench_r2b.json 2> gpurun_out/bench_r2b.err; echo rc=$? >> gpurun_out/bench_r2b.err
+python -m pytest tests -m gpu -x -q > gpurun_out/tq.log 2>&1; echo rc=$? >> gpurun_out/tq.log
+python tools/timing_check.py > gpurun_out/tkq.log 2>&1
