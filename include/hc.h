@@ -100,7 +100,7 @@ typedef enum hc_path {
     HC_PATH_AUTO = 0,   /* chosen from m, q */
     HC_PATH_STAGED = 1, /* text tiles staged in shared memory by TMA bulk copies */
     HC_PATH_GATHER = 2, /* no staging: lanes read only the q-grams they hash, from global memory */
-    HC_PATH_STREAM = 3, /* per-warp chunks staged in shared memory by 16-byte cp.async copies */
+    HC_PATH_STREAM = 3, /* per-warp chunks staged in shared memory by 1-D TMA bulk copies */
     HC_PATH_SHC = 4,    /* Sentinel Hash Chain (Fig. 5 right): per-lane ranges copied into shared-
                            memory boxes followed by a copy of x, SHC's fast loop per lane */
     HC_PATH_SCAN = 5    /* hash every position of staged pieces once into filter / link bitmaps,
@@ -112,7 +112,8 @@ typedef struct hc_search_opts {
     int tile_bytes;   /* staged: text bytes per shared-memory stage; stream: target text bytes
                          per warp chunk (0 = default) */
     int stages;       /* staged: TMA pipeline depth; stream: buffers per warp, 2..4 (0 = default 2) */
-    int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default) */
+    int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default);
+                         stream: < 0 = final drain on global text (no private boxes) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
     int time_kernel;  /* 1: record CUDA events around this call's device work (stats->kernel_ms);
                          2: also around the search kernel alone (stats->search_ms; the extra
@@ -123,8 +124,8 @@ typedef struct hc_search_opts {
                          valid) exist only in the instrumented build libhc_instr.so
                          (HC_INSTRUMENT=1, tools/); this library returns HC_EINVAL if set */
     int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage);
-                         stream: > 0 = each chunk by one 1-D TMA bulk copy instead of
-                         16-byte cp.async per lane */
+                         stream: < 0 = chunks by 16-byte cp.async per lane instead of one
+                         1-D TMA bulk copy per chunk (the default) */
     unsigned long long *trace; /* must be NULL (instrumented build only: DEVICE buffer of
                                   grid x trace_tiles x 4 %globaltimer stamps per (CTA, tile)) */
     int trace_tiles;

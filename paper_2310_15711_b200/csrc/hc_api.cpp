@@ -37,6 +37,9 @@ struct hc_handle {
     uint32_t *dF = nullptr;        // device image: F | filter bitmap | x (zero-padded)
     uint32_t *dFbits = nullptr;
     uint8_t *dx = nullptr;
+    uint16_t *dFrank = nullptr;    // ... | rank table | compact F (stream path)
+    uint32_t *dFc = nullptr;
+    uint32_t nfc = 0;              // non-empty words of F
     std::shared_ptr<void> block;   // hc_prepare_batch: device block shared by the batch
 };
 
@@ -88,27 +91,44 @@ void build_table(const uint8_t *x, uint32_t m, uint32_t q, uint32_t alpha, uint3
 
 // Device image of a handle's table, one allocation: F (2^alpha words) | the filter bitmap
 // (bit v set iff F[v] != 0: the l.6 test of Fig. 5 alone, 2^alpha bits, at least 16 B) |
-// x followed by at least 24 zero bytes.  Each part starts 16-byte aligned and has a
-// size that is a multiple of 16, so the kernels can move F and x with 1-D TMA bulk copies
-// and 16-byte loads without reading past the image.
+// x followed by at least 24 zero bytes | the rank table (u16 per bitmap word: non-empty
+// words of F below it) | compact F (the non-empty words of F in order of v; at most
+// min(m, 2^alpha)).  The last two serve the stream path, which keeps the bitmap (one copy
+// per lane), the rank table and compact F in shared memory instead of F: F[v] =
+// bit v ? Fc[rank[v >> 5] + popc(bitmap word below bit v)] : 0.  Each part starts 16-byte
+// aligned and has a size that is a multiple of 16, so the kernels can move F and x with
+// 1-D TMA bulk copies and 16-byte loads without reading past the image.
 struct ImageLayout {
-    size_t f_off, bits_off, x_off, bytes;
+    size_t f_off, bits_off, x_off, rank_off, fc_off, bytes;
 };
 ImageLayout image_layout(uint32_t alpha, size_t m) {
     ImageLayout L;
     const size_t fbytes = (size_t(1) << alpha) * sizeof(uint32_t);
+    const size_t nwords = std::max<size_t>(1, (size_t(1) << alpha) / 32);
+    const size_t nfc = std::min<size_t>(m, size_t(1) << alpha);
     L.f_off = 0;
     L.bits_off = (fbytes + 15) & ~size_t(15);
     L.x_off = L.bits_off + std::max<size_t>(16, ((size_t(1) << alpha) / 8 + 15) & ~size_t(15));
-    L.bytes = L.x_off + ((m + 24 + 15) & ~size_t(15));
+    L.rank_off = L.x_off + ((m + 24 + 15) & ~size_t(15));
+    L.fc_off = L.rank_off + ((nwords * 2 + 15) & ~size_t(15));
+    L.bytes = L.fc_off + std::max<size_t>(16, (nfc * 4 + 15) & ~size_t(15));
     return L;
 }
-void write_image(const hc_handle *h, uint8_t *dst) {   // dst: image_layout(...).bytes, zeroed
+void write_image(hc_handle *h, uint8_t *dst) {   // dst: image_layout(...).bytes, zeroed
     const ImageLayout L = image_layout(h->alpha, h->m);
     std::memcpy(dst + L.f_off, h->F.data(), h->F.size() * sizeof(uint32_t));
     uint32_t *bits = reinterpret_cast<uint32_t *>(dst + L.bits_off);
-    for (size_t v = 0; v < h->F.size(); ++v)
-        if (h->F[v]) bits[v >> 5] |= 1u << (v & 31);
+    uint16_t *rank = reinterpret_cast<uint16_t *>(dst + L.rank_off);
+    uint32_t *fc = reinterpret_cast<uint32_t *>(dst + L.fc_off);
+    uint32_t cnt = 0;
+    for (size_t v = 0; v < h->F.size(); ++v) {
+        if ((v & 31) == 0) rank[v >> 5] = static_cast<uint16_t>(cnt);
+        if (h->F[v]) {
+            bits[v >> 5] |= 1u << (v & 31);
+            fc[cnt++] = h->F[v];
+        }
+    }
+    h->nfc = cnt;
     std::memcpy(dst + L.x_off, h->x.data(), h->m);
 }
 void bind_image(hc_handle *h, uint8_t *base) {
@@ -116,6 +136,8 @@ void bind_image(hc_handle *h, uint8_t *base) {
     h->dF = reinterpret_cast<uint32_t *>(base + L.f_off);
     h->dFbits = reinterpret_cast<uint32_t *>(base + L.bits_off);
     h->dx = base + L.x_off;
+    h->dFrank = reinterpret_cast<uint16_t *>(base + L.rank_off);
+    h->dFc = reinterpret_cast<uint32_t *>(base + L.fc_off);
 }
 
 // Per-host-thread, per-device scratch: [kCtr counter words | positions (cap u32)] plus
@@ -274,6 +296,9 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
     p.n = nn;
     p.F = h->dF;
     p.Fbits = h->dFbits;
+    p.Frank = h->dFrank;
+    p.Fc = h->dFc;
+    p.nfc = h->nfc;
     p.x = h->dx;
     p.m = m;
     p.q = q;
@@ -342,6 +367,14 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         p.stages = o.stages >= 2 && o.stages <= 4 ? static_cast<uint32_t>(o.stages) : kDefaultStreamBufs;
         p.block_warps = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps)
                                                                   : kDefaultStreamWarps;
+        // chunks move by one 1-D TMA bulk copy each (tma_chunk < 0: 16-byte cp.async per lane)
+        p.tma_chunk = o.tma_chunk < 0 ? 0u : 1u;
+        // final drain on private boxes (hc_stream.cu): 16 bytes of slack + the segment's reach
+        // m + S - 1 in whole 16-byte words, one box per lane in the warp's idle chunk buffers
+        {
+            const uint32_t slot = 16 + ((m + S - 1 + 30 + 15) & ~15u);
+            p.slot_bytes = 32 * slot <= p.stages * p.stage_bytes && o.seg_per_lane >= 0 ? slot : 0u;
+        }
         // shifts too long for per-warp buffers (S > ~200) take the gather path, which
         // reads only the q-grams it hashes anyway
         if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps) >

@@ -124,6 +124,17 @@ __device__ __forceinline__ void trace_cta(const KParams &p, uint32_t ev) {
     if (kInstrument && p.trace)
         p.trace[static_cast<size_t>(gridDim.x) * p.trace_tiles * 4 + blockIdx.x * 2 + ev] = gtimer();
 }
+// debug 12 (instrumented build): latest time any warp passed point i of the search's
+// critical path (point 0: earliest CTA entry, stored complemented), kept after the
+// per-CTA records of the trace buffer
+__device__ __forceinline__ void path_ts(const KParams &p, uint32_t i) {
+    if (kInstrument && p.trace && p.debug == 12 && (threadIdx.x & 31) == 0) {
+        unsigned long long *a =
+            p.trace + static_cast<size_t>(gridDim.x) * (p.trace_tiles * 4 + 2) + 8 + i;
+        const unsigned long long t = gtimer();
+        atomicMax(a, i == 0 ? ~t : t);
+    }
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -220,6 +231,54 @@ struct FBits {
     }
 };
 
+// Stream path: the filter bitmap replicated per lane in shared memory (word (v >> 5) of
+// lane l's copy at word index (v >> 5) * 32 + l, i.e. in bank l), so the l.6 test of 32
+// random hash values never conflicts (the same lookups in F: ~5 wavefronts per load on
+// DNA, measured 6 us of a 64 us search at m = 16 and 13 us of 88 at m = 8).  Same size as
+// F (2^alpha words), which it replaces in shared memory.  The survivors' F words come
+// from compact F (the <= S non-empty words in order of v) through the rank table:
+// F[v] = bit v ? Fc[rank[v >> 5] + popc(bits of the word below v)] : 0.
+struct LaneBitsF {
+    uint32_t col;          // shared addresses: this lane's bitmap column (table + 4 * lane),
+    uint32_t rank, fc;     // the rank table (u16 per bitmap word) and compact F
+    __device__ __forceinline__ bool pass(uint32_t v) const {
+        return (lds32(col + ((v >> 5) << 7)) >> (v & 31)) & 1u;
+    }
+    __device__ __forceinline__ uint32_t operator[](uint32_t v) const {
+        const uint32_t w = lds32(col + ((v >> 5) << 7)), b = v & 31;
+        uint32_t z = 0;
+        if ((w >> b) & 1u) {
+            uint32_t r;
+            asm("ld.shared.u16 %0, [%1];" : "=r"(r) : "r"(rank + 2 * (v >> 5)));
+            z = lds32(fc + 4 * (r + __popc(w & ((1u << b) - 1u))));
+        }
+        return z;
+    }
+};
+// builds the per-lane copies from the global bitmap (2^alpha bits, >= 4 words), whole CTA
+__device__ __forceinline__ void load_lane_bits(const KParams &p, uint32_t *tab) {
+    const uint32_t nw = (1u << p.alpha) > 32 ? (1u << p.alpha) / 32 : 1u;
+    for (uint32_t i0 = threadIdx.x; i0 < nw * 32; i0 += 8 * blockDim.x) {
+        uint32_t v[8];
+#pragma unroll
+        for (uint32_t r = 0; r < 8; ++r) {
+            const uint32_t i = i0 + r * blockDim.x;
+            if (i < nw * 32) v[r] = __ldg(p.Fbits + (i >> 5));
+        }
+#pragma unroll
+        for (uint32_t r = 0; r < 8; ++r) {
+            const uint32_t i = i0 + r * blockDim.x;
+            if (i < nw * 32) tab[i] = v[r];
+        }
+    }
+}
+// the rank table and compact F of the image, into shared memory (whole CTA)
+__device__ __forceinline__ void load_rank_fc(const KParams &p, uint16_t *srank, uint32_t *sfc) {
+    const uint32_t nw = (1u << p.alpha) > 32 ? (1u << p.alpha) / 32 : 1u;
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) srank[i] = __ldg(p.Frank + i);
+    for (uint32_t i = threadIdx.x; i < p.nfc; i += blockDim.x) sfc[i] = __ldg(p.Fc + i);
+}
+
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
 // top Q bytes are meaningful.  Reads just the aligned 8-byte words holding y[p]
 // and y[p-Q+1] (both inside the text).  On global text such a word can extend up to
@@ -290,15 +349,28 @@ __device__ __forceinline__ uint32_t qhash(uint64_t W, uint32_t mask) {
 // shared memory, 16-aligned).  8 bytes per step, then a byte tail.
 template <class T>
 __device__ __noinline__ bool verify(const T &t, const uint8_t *sx, uint32_t start, uint32_t m) {
-    uint32_t k = 0;
-    for (; k + 8 <= m; k += 8) {
-        const uint64_t a = end8<8>(t, start + k + 7);
-        const uint64_t b = *reinterpret_cast<const uint64_t *>(sx + k);
-        if (a != b) return false;
+    // 8-byte words, four loads in flight per round (one memory round trip per 32 bytes, not
+    // one per word); the last m % 8 bytes by an overlapping word (m >= 8) or bytewise
+    uint64_t bad = 0;
+    if (m >= 8 && (m & 7u)) {
+        const uint32_t o = m - 8, sh = 8 * (o & 7u);
+        const uint64_t *w = reinterpret_cast<const uint64_t *>(sx + (o & ~7u));
+        const uint64_t b = shr64(w[0], sh) | shl64(w[1], 64 - sh);   // x[m-8 .. m-1], sh > 0
+        bad = end8<8>(t, start + m - 1) ^ b;
     }
-    for (; k < m; ++k)
-        if (t.byte(start + k) != sx[k]) return false;
-    return true;
+    for (uint32_t k = 0; k + 8 <= m; k += 32) {
+        uint64_t a[4];
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) a[r] = k + 8 * r + 8 <= m ? end8<8>(t, start + k + 8 * r + 7) : 0ull;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r)
+            if (k + 8 * r + 8 <= m) bad |= a[r] ^ *reinterpret_cast<const uint64_t *>(sx + k + 8 * r);
+        if (bad) return false;
+    }
+    if (m < 8)
+        for (uint32_t k = 0; k < m; ++k)
+            if (t.byte(start + k) != sx[k]) return false;
+    return bad == 0;
 }
 
 // The same comparison done by the whole warp, 4 x 8 bytes per lane per round.
@@ -741,6 +813,7 @@ struct WarpQueueSink {
 
 __host__ __device__ inline uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
+__device__ __forceinline__ void load_x(const KParams &p, uint8_t *sx);
 __device__ __forceinline__ void load_table(const KParams &p, uint32_t *sF, uint8_t *sx) {
     // F (2^alpha words) and x, with every thread's loads issued before its stores: one
     // L2 round trip for the whole table instead of one per loop trip
@@ -765,6 +838,9 @@ __device__ __forceinline__ void load_table(const KParams &p, uint32_t *sF, uint8
     } else {
         for (uint32_t w = threadIdx.x; w < nF; w += blockDim.x) sF[w] = __ldg(p.F + w);
     }
+    load_x(p, sx);
+}
+__device__ __forceinline__ void load_x(const KParams &p, uint8_t *sx) {
     // x in 16-byte vectors (the device copy of x has >= 15 readable bytes past m), with
     // the bytes from m on zeroed up to m + 8 so that 8-byte compares of x never read
     // uninitialised shared memory
@@ -1108,7 +1184,9 @@ inline uint32_t epi_cap_for(int smem_bytes) {
 
 // Single-pattern kernels: the epilogue of search p (call from every thread at the end).
 __device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem) {
-    if (!cta_is_last(p.counter + 2)) return;
+    const bool last_cta = cta_is_last(p.counter + 2);
+    path_ts(p, 7);
+    if (!last_cta) return;
     if (*reinterpret_cast<volatile uint32_t *>(p.counter + 3)) {
         // the search gave up (walk-heavy text, see gather_kernel): the host re-runs it on
         // the scan path; nothing of this run is published but the verdict
@@ -1123,6 +1201,7 @@ __device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem)
                    p.debug == 9);
     __syncthreads();
     if (threadIdx.x == 0) p.counter[2] = 0;
+    path_ts(p, 8);
 }
 
 // ------------------------------------------------------------------ launch helpers

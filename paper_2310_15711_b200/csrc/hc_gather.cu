@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Lo.bar_off);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (kInstrument && tid == 0) trace_cta(p, 0);
+    path_ts(p, 0);
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
                                           reinterpret_cast<uint32_t *>(smem + Lo.q2_off) + warp * kWarpBuf,
                                           0u, 0u, wo, lane};
     bool ready = false;
+    path_ts(p, 1);
     if (kInstrument && lane == 0) trace_event(p, warp, 0);          // bitmap loaded
     if (L >= 4)
         gather_loop<Q, SH, 4>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
@@ -131,11 +133,15 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
         gather_loop<Q, SH, 2>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
     else
         gather_loop<Q, SH, 1>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
+    path_ts(p, 3);
     if (!ready) mbar_wait(bar, 0);
+    path_ts(p, 4);
     if (kInstrument && lane == 0) trace_event(p, warp, 1);          // lattice filtered
     sink.drain();
+    path_ts(p, 5);
     if (kInstrument && lane == 0) trace_event(p, warp, 2);          // survivors done
     wo.flush(p, lane);
+    path_ts(p, 6);
     if (kInstrument && lane == 0) trace_event(p, warp, 3);          // flushed
     if (kInstrument && lane == 0) trace_cta(p, 1);   // last warp to get here wins
     __syncthreads();

@@ -14,6 +14,9 @@ struct KParams {
     uint32_t n;          // text length (n >= m, n <= HC_MAX_TEXT)
     const uint32_t *F;   // filter table, device, 2^alpha words
     const uint32_t *Fbits;  // filter bitmap, device, 2^alpha bits (bit v = F[v] != 0), >= 16 B
+    const uint16_t *Frank;  // per bitmap word: non-empty words of F below it (stream path)
+    const uint32_t *Fc;     // the nfc non-empty words of F in order of v (stream path)
+    uint32_t nfc;
     const uint8_t *x;    // pattern, device, followed by >= 24 zero bytes (16-byte aligned)
     uint32_t m, q, s, mask, hv;
     uint32_t S;          // shift m - q + 1: also the segment length

@@ -20,14 +20,16 @@ namespace hc {
 // buffer; the lattice survivors go through first_steps and phase B on global text
 // (the chunk was just streamed through L2), exactly as on the gather path.
 struct StreamLayout {
-    uint32_t f_off, x_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
+    uint32_t f_off, x_off, rank_off, fc_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
 };
 __host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m, uint32_t nwarps,
                                                       uint32_t buf_bytes, uint32_t bufs) {
     StreamLayout L;
     L.f_off = 0;
-    L.x_off = round_up((1u << alpha) * 4u, 16);
-    L.q_off = L.x_off + round_up(m + 8, 16);
+    L.x_off = round_up(max((1u << alpha) * 4u, 128u), 16);   // the per-lane filter bitmaps
+    L.rank_off = L.x_off + round_up(m + 8, 16);
+    L.fc_off = L.rank_off + round_up(2u * max((1u << alpha) / 32u, 1u), 16);
+    L.q_off = L.fc_off + round_up(4u * min(m, 1u << alpha), 16);
     L.q2_off = L.q_off + nwarps * kStreamQ1 * 4u;
     L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
     L.ctr_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
@@ -54,7 +56,7 @@ struct StreamQueue {
     // first steps of 32 queued survivors, on the chunk's stage (the queue only ever
     // holds survivors of the chunk being filtered: it is drained at the chunk's end)
     template <class TT>
-    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText> &sink,
+    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
                                             const TT &txt, uint32_t lane) {
         __syncwarp();
         const uint32_t e = q1[n1 - 32 + lane];
@@ -65,7 +67,7 @@ struct StreamQueue {
         sink.steps_e_on(txt, true, e);
     }
     template <class TT>
-    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText> &sink,
+    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
                                               const TT &txt, uint32_t lane) {
         while (n1 >= 32) drain32(sink, txt, lane);
         if (n1) {
@@ -82,10 +84,10 @@ struct StreamQueue {
 };
 
 template <int Q, int SH>
-__device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &txt, const FTable &sF,
+__device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &txt, const LaneBitsF &sF,
                                               uint32_t k0, uint32_t k1, uint32_t lane,
                                               StreamQueue<Q, SH> &qu,
-                                              WarpQueueSink<Q, SH, GlobalText> &sink) {
+                                              WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink) {
     const uint32_t step = 32 * p.S;
     uint32_t pos = p.m - 1 + (k0 + lane) * p.S;   // window end a_k of lattice point k0 + lane
     uint32_t k = k0;
@@ -94,14 +96,23 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             uint64_t W[kStreamUnroll];
 #pragma unroll
             for (int u = 0; u < kStreamUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
-            uint32_t pm = 0;
+            if (kInstrument && p.debug == 14)          // no text loads (measurement)
 #pragma unroll
-            for (int u = 0; u < kStreamUnroll; ++u)
-                pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
-            if (kInstrument && p.debug == 3) pm = 0;   // phase A alone (measurement)
-            const uint32_t c = __popc(pm);
-            const uint32_t tot = __reduce_add_sync(HC_FULL, c);
-            if (tot) {
+                for (int u = 0; u < kStreamUnroll; ++u) W[u] = (pos + u * step) * 0x9E3779B97F4A7C15ull;
+            uint32_t pm = 0;
+            if (kInstrument && p.debug == 13) {        // no F lookups (measurement)
+#pragma unroll
+                for (int u = 0; u < kStreamUnroll; ++u)
+                    pm |= static_cast<uint32_t>(qhash<Q, SH>(W[u], p.mask) == 0xfffffu) << u;
+            } else {
+#pragma unroll
+                for (int u = 0; u < kStreamUnroll; ++u)
+                    pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
+            }
+            if (kInstrument && (p.debug == 3 || p.debug == 14)) pm = 0;   // phase A alone (measurement)
+            if (__any_sync(HC_FULL, pm != 0)) {
+                const uint32_t c = __popc(pm);
+                const uint32_t tot = __reduce_add_sync(HC_FULL, c);
                 if (c) {
                     uint32_t slot = atomicAdd(qu.ctr, c);
 #pragma unroll
@@ -138,14 +149,21 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
     }
 }
 
+// cp.async variant (opts.tma_chunk < 0): 16-byte cp.async per lane; the first NB - 1
+// chunks were issued by the kernel's prologue (before the table load).
+template <int NB>
+__device__ __forceinline__ void stream_prologue(const KParams &p, uint32_t bufs0, uint32_t gw,
+                                                uint32_t total_warps, uint32_t lane) {
+#pragma unroll
+    for (int b = 0; b < NB - 1; ++b)
+        stream_issue(p, gw + b * total_warps, bufs0 + b * p.stage_bytes, lane);
+}
 template <int Q, int SH, int NB>
-__device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
-                                            WarpQueueSink<Q, SH, GlobalText> &sink,
+__device__ __forceinline__ void stream_loop(const KParams &p, const LaneBitsF &sF,
+                                            WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
                                             StreamQueue<Q, SH> &qu, uint32_t bufs0,
                                             uint32_t gw, uint32_t total_warps, uint32_t lane) {
     const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
-#pragma unroll
-    for (int b = 0; b < NB - 1; ++b) stream_issue(p, gw + b * total_warps, bufs0 + b * p.stage_bytes, lane);
     uint32_t b = 0;
     for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
         // refill the buffer filtered last round with the chunk NB-1 ahead
@@ -168,69 +186,153 @@ __device__ __forceinline__ void stream_loop(const KParams &p, const FTable &sF,
     cp_async_wait<0>();
 }
 
-// The same loop with each chunk moved by ONE 1-D TMA bulk copy (cp.async.bulk, issued
-// by lane 0, completion on the buffer's mbarrier) instead of 16-byte cp.async per lane;
-// the partial 16-byte words at the two ends of an unaligned text are stored by the
-// lanes (first / last chunk only).
-template <int Q, int SH, int NB>
-__device__ __forceinline__ void stream_loop_tma(const KParams &p, const FTable &sF,
-                                                WarpQueueSink<Q, SH, GlobalText> &sink,
-                                                StreamQueue<Q, SH> &qu, uint32_t bufs0, uint64_t *bar,
-                                                uint32_t gw, uint32_t total_warps, uint32_t lane) {
-    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
-    const uintptr_t y = reinterpret_cast<uintptr_t>(p.y), ye = y + p.n;
+// TMA variant (the default): each chunk moved by ONE 1-D bulk copy (cp.async.bulk, issued
+// by lane 0, completion on the buffer's mbarrier).  Interior chunks (all but the first and
+// the last few of the text) have a fixed geometry: chunk c holds lattice points
+// [c spc, (c+1) spc) and text bytes [first, first + D + max(q, 2q - S)), first = c D + m - 2q,
+// D = spc S (stream_chunk's range, unclipped), so the loop only advances `first`; their 16-byte words lie wholly inside y.  Edge chunks
+// take the general route (stream_chunk; the partial 16-byte words at the two ends of an
+// unaligned text are stored by the lanes).
+struct TmaStream {
+    uintptr_t y;
+    uint32_t y32, D, len, bufs0, stage_bytes;
+    uint64_t *bar;
+};
+__device__ __forceinline__ bool chunk_interior(const KParams &p, const TmaStream &ts, uint32_t c,
+                                               uint32_t first) {
+    return c >= 1 && first + ts.len + 15 <= p.n;
+}
+__device__ __forceinline__ void tma_issue(const KParams &p, const TmaStream &ts, uint32_t c,
+                                          uint32_t first, uint32_t b, uint32_t lane) {
+    if (c >= p.nchunks) return;
+    const uint32_t buf = ts.bufs0 + b * ts.stage_bytes;
+    if (chunk_interior(p, ts, c, first)) {
+        if (lane == 0) {
+            const uintptr_t A = (ts.y + first) & ~static_cast<uintptr_t>(15);
+            const uint32_t bytes = (((ts.y32 + first) & 15u) + ts.len + 15u) & ~15u;
+            mbar_arrive_expect_tx(&ts.bar[b], bytes);
+            bulk_g2s(buf, reinterpret_cast<const void *>(A), bytes, &ts.bar[b]);
+        }
+        return;
+    }
+    const uintptr_t y = ts.y, ye = y + p.n;
+    const StreamChunk g = stream_chunk(p, c);
+    const uintptr_t A = (y + g.first) & ~static_cast<uintptr_t>(15);
+    const uint32_t nbytes = static_cast<uint32_t>(((y + g.last + 16) & ~static_cast<uintptr_t>(15)) - A);
+    const uintptr_t lo = max(A, (y + 15) & ~static_cast<uintptr_t>(15));
+    const uintptr_t hi = min(A + nbytes, ye & ~static_cast<uintptr_t>(15));
+    if (A < lo || A + nbytes > hi) {                 // bytes outside [lo, hi)
+        for (uintptr_t a = A + lane; a < A + nbytes; a += 32)
+            if ((a < lo || a >= hi) && a >= y && a < ye)
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + static_cast<uint32_t>(a - A)),
+                             "r"(static_cast<uint32_t>(__ldg(reinterpret_cast<const uint8_t *>(a))))
+                             : "memory");
+    }
+    __syncwarp();
     if (lane == 0) {
-        for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+        fence_proxy_async();                         // the lanes' stores above
+        if (hi > lo) {
+            mbar_arrive_expect_tx(&ts.bar[b], static_cast<uint32_t>(hi - lo));
+            bulk_g2s(buf + static_cast<uint32_t>(lo - A), reinterpret_cast<const void *>(lo),
+                     static_cast<uint32_t>(hi - lo), &ts.bar[b]);
+        } else {
+            mbar_arrive(&ts.bar[b]);
+        }
+    }
+}
+template <int NB>
+__device__ __forceinline__ void stream_prologue_tma(const KParams &p, const TmaStream &ts, uint32_t gw,
+                                                    uint32_t total_warps, uint32_t lane) {
+    if (lane == 0) {
+        for (int b = 0; b < NB; ++b) mbar_init(&ts.bar[b], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](uint32_t c, uint32_t b) {
-        if (c >= p.nchunks) return;
-        const StreamChunk g = stream_chunk(p, c);
-        const uintptr_t A = (y + g.first) & ~static_cast<uintptr_t>(15);
-        const uint32_t nbytes =
-            static_cast<uint32_t>(((y + g.last + 16) & ~static_cast<uintptr_t>(15)) - A);
-        const uint32_t buf = bufs0 + b * p.stage_bytes;
-        const uintptr_t lo = max(A, (y + 15) & ~static_cast<uintptr_t>(15));
-        const uintptr_t hi = min(A + nbytes, ye & ~static_cast<uintptr_t>(15));
-        if (A < lo || A + nbytes > hi) {                 // edge chunk: bytes outside [lo, hi)
-            for (uintptr_t a = A + lane; a < A + nbytes; a += 32)
-                if ((a < lo || a >= hi) && a >= y && a < ye)
-                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + static_cast<uint32_t>(a - A)),
-                                 "r"(static_cast<uint32_t>(__ldg(reinterpret_cast<const uint8_t *>(a))))
-                                 : "memory");
-        }
-        __syncwarp();
-        if (lane == 0) {
-            fence_proxy_async();                         // earlier generic reads of the buffer
-            if (hi > lo) {
-                mbar_arrive_expect_tx(&bar[b], static_cast<uint32_t>(hi - lo));
-                bulk_g2s(buf + static_cast<uint32_t>(lo - A), reinterpret_cast<const void *>(lo),
-                         static_cast<uint32_t>(hi - lo), &bar[b]);
-            } else {
-                mbar_arrive(&bar[b]);
-            }
-        }
-    };
 #pragma unroll
-    for (int b = 0; b < NB - 1; ++b) issue(gw + b * total_warps, b);
+    for (int b = 0; b < NB - 1; ++b) {
+        const uint32_t c = gw + b * total_warps;
+        tma_issue(p, ts, c, c * ts.D + p.m - 2 * p.q, b, lane);
+    }
+}
+template <int Q, int SH, int NB>
+__device__ __forceinline__ void stream_loop_tma(const KParams &p, const LaneBitsF &sF,
+                                                WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
+                                                StreamQueue<Q, SH> &qu, const TmaStream &ts,
+                                                uint32_t gw, uint32_t total_warps, uint32_t lane) {
+    const uint32_t stride = total_warps * ts.D;
+    uint32_t first = gw * ts.D + p.m - 2 * p.q;       // of chunk c when interior (mod 2^32)
     uint32_t b = 0, par = 0;   // par: bit b = phase parity of buffer b's next completion
-    for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
+    for (uint32_t c = gw; c < p.nchunks; c += total_warps, first += stride) {
         const uint32_t bn = b == 0 ? NB - 1 : b - 1;
-        issue(c + (NB - 1) * total_warps, bn);
-        mbar_wait(&bar[b], (par >> b) & 1u);
+        tma_issue(p, ts, c + (NB - 1) * total_warps, first + (NB - 1) * stride, bn, lane);
+        mbar_wait(&ts.bar[b], (par >> b) & 1u);
         par ^= 1u << b;
-        const StreamChunk g = stream_chunk(p, c);
-        const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
-        const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
+        const uint32_t buf = fence_value(ts.bufs0 + b * ts.stage_bytes);
         if (!(kInstrument && p.debug == 1)) {   // debug 1: copy pipeline alone
-            stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
+            uint32_t k0 = c * p.seg_per_chunk, k1 = k0 + p.seg_per_chunk, f = first;
+            if (!chunk_interior(p, ts, c, first)) {
+                const StreamChunk g = stream_chunk(p, c);
+                k1 = g.k1;
+                f = g.first;
+            }
+            const SmemText txt{buf + ((ts.y32 + f) & 15u) - f};
+            stream_filter<Q, SH>(p, txt, sF, k0, k1, lane, qu, sink);
 #if !HC_STREAM_GLOBAL_FS
             qu.drain_all(sink, txt, lane);
 #endif
         }
-        __syncwarp();
+        __syncwarp();              // every lane is done with buffer b before its refill
         b = b + 1 == NB ? 0 : b + 1;
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (int i = 0; i < NB; ++i) mbar_inval(&ts.bar[i]);   // the epilogue reuses this memory
+}
+
+// Final drain on private copies.  When a warp runs out of chunks its queues still hold
+// < 32 lattice survivors (q1) and < 32 continuing segments (q2).  Running them through
+// first steps and phase B on global text is a chain of dependent L2 round trips (one per
+// window visited, up to ~10 for the slowest warp: 5-6 us at the end of every search, when
+// nothing else is left to overlap it).  Instead each lane copies the text its segment can
+// ever touch, y[a_k - m + 1 .. a_k + S - 1] (R11), into a private box in the warp's now
+// idle chunk buffers (one round trip for all of them), and Fig. 5 continues on the box at
+// shared-memory latency.  A lattice survivor starts at its window end a_k (first_steps is
+// only a shortcut of the same loop).  p.slot_bytes = box size (0: boxes do not fit).
+template <int Q, int SH>
+__device__ __forceinline__ void final_drain_boxes(const KParams &p, const LaneBitsF &sF, const uint8_t *sx,
+                                                  const uint32_t *q1, uint32_t n1, const uint32_t *q2,
+                                                  uint32_t n2, uint32_t boxes, WarpOut &wo, uint32_t lane) {
+    const uintptr_t y = reinterpret_cast<uintptr_t>(p.y), ye = y + p.n;
+    const uint32_t total = n1 + n2;
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t idx = base + lane;
+        const bool act = idx < total;
+        const uint32_t start = act ? (idx < n1 ? q1[idx] : q2[idx - n1]) : p.m - 1;
+        const uint32_t ak = p.m - 1 + (start - (p.m - 1)) / p.S * p.S;
+        const uint32_t lo = ak + 1 - p.m, hi = min(ak + p.S, p.n) - 1;
+        const uint32_t box = boxes + lane * p.slot_bytes + 16;   // 16 bytes of slack below (end8)
+        const uintptr_t A = (y + lo) & ~static_cast<uintptr_t>(15);
+        const uintptr_t B = (y + hi + 16) & ~static_cast<uintptr_t>(15);
+        if (act) {
+            for (uintptr_t w = A; w < B; w += 16) {
+                const uint32_t d = box + static_cast<uint32_t>(w - A);
+                if (w >= y && w + 16 <= ye) {
+                    cp_async16(d, reinterpret_cast<const void *>(w));
+                } else {
+                    for (uint32_t b = 0; b < 16; ++b)
+                        if (w + b >= y && w + b < ye)
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(d + b),
+                                         "r"(static_cast<uint32_t>(__ldg(reinterpret_cast<const uint8_t *>(w + b))))
+                                         : "memory");
+                }
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        const SmemText txt{fence_value(box + static_cast<uint32_t>((y + lo) - A)) - lo};
+        run_segments<Q, SH>(p, txt, sF, sx, act, start, wo, lane);
+        __syncwarp();
     }
 }
 
@@ -248,17 +350,35 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
     uint8_t *sx = smem + L.x_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (kInstrument && tid == 0) trace_cta(p, 0);
+    path_ts(p, 0);
     pdl_launch_dependents();
     const uint32_t total_warps = gridDim.x * NW;
     const uint32_t gw = blockIdx.x * NW + warp;
     const uint32_t bufs0 = smem_u32(smem + L.buf_off) + warp * p.stages * p.stage_bytes;
-    load_table(p, sFp, sx);
+    // the first chunks' copies go out before the table load: both DRAM round trips overlap
+    const uintptr_t yaddr = reinterpret_cast<uintptr_t>(p.y);
+    const TmaStream ts{yaddr, static_cast<uint32_t>(yaddr), p.seg_per_chunk * p.S,
+                       p.seg_per_chunk * p.S + max(p.q, 2 * p.q - min(p.S, 2 * p.q)), bufs0, p.stage_bytes,
+                       reinterpret_cast<uint64_t *>(smem + L.ctr_off + round_up(NW * 4u, 8)) + warp * 4};
+    if (p.tma_chunk) {
+        if (p.stages == 4) stream_prologue_tma<4>(p, ts, gw, total_warps, lane);
+        else if (p.stages == 3) stream_prologue_tma<3>(p, ts, gw, total_warps, lane);
+        else stream_prologue_tma<2>(p, ts, gw, total_warps, lane);
+    } else if (p.stages == 2) stream_prologue<2>(p, bufs0, gw, total_warps, lane);
+    else if (p.stages == 3) stream_prologue<3>(p, bufs0, gw, total_warps, lane);
+    else stream_prologue<4>(p, bufs0, gw, total_warps, lane);
+    load_lane_bits(p, sFp);
+    load_rank_fc(p, reinterpret_cast<uint16_t *>(smem + L.rank_off),
+                 reinterpret_cast<uint32_t *>(smem + L.fc_off));
+    load_x(p, sx);
     if (tid == 0) s_params[0] = p;
     __syncthreads();
-    const FTable sF{fence_value(smem_u32(sFp))};
+    path_ts(p, 1);
+    const LaneBitsF sF{fence_value(smem_u32(sFp)) + 4 * lane, smem_u32(smem + L.rank_off),
+                       smem_u32(smem + L.fc_off)};
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const GlobalText gtxt{p.y};
-    WarpQueueSink<Q, SH, GlobalText> sink{p, gtxt, sF, sx, nullptr,
+    WarpQueueSink<Q, SH, GlobalText, LaneBitsF> sink{p, gtxt, sF, sx, nullptr,
                                           reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
                                           0u, 0u, wo, lane};
     uint32_t *ctr = reinterpret_cast<uint32_t *>(smem + L.ctr_off) + warp;
@@ -266,22 +386,34 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
     __syncwarp();
     StreamQueue<Q, SH> qu{reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kStreamQ1, ctr, 0u};
     if (p.tma_chunk) {
-        uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.ctr_off + round_up(NW * 4u, 8)) + warp * 4;
-        if (p.stages == 3)
-            stream_loop_tma<Q, SH, 3>(p, sF, sink, qu, bufs0, bar, gw, total_warps, lane);
+        if (p.stages == 4)
+            stream_loop_tma<Q, SH, 4>(p, sF, sink, qu, ts, gw, total_warps, lane);
+        else if (p.stages == 3)
+            stream_loop_tma<Q, SH, 3>(p, sF, sink, qu, ts, gw, total_warps, lane);
         else
-            stream_loop_tma<Q, SH, 2>(p, sF, sink, qu, bufs0, bar, gw, total_warps, lane);
+            stream_loop_tma<Q, SH, 2>(p, sF, sink, qu, ts, gw, total_warps, lane);
     } else if (p.stages == 2)
         stream_loop<Q, SH, 2>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
     else if (p.stages == 3)
         stream_loop<Q, SH, 3>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
     else
         stream_loop<Q, SH, 4>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+    path_ts(p, 3);
+    if (p.slot_bytes) {
+        __syncwarp();
+        final_drain_boxes<Q, SH>(p, sF, sx, qu.q1, qu.n1, sink.q2, sink.n2, bufs0, wo, lane);
+        qu.n1 = 0;
+        sink.n2 = 0;
+    } else {
 #if HC_STREAM_GLOBAL_FS
-    qu.drain_all(sink, gtxt, lane);
+        qu.drain_all(sink, gtxt, lane);
 #endif
-    sink.drain();
+        path_ts(p, 4);
+        sink.drain();
+    }
+    path_ts(p, 5);
     wo.flush(p, lane);
+    path_ts(p, 6);
     if (kInstrument && lane == 0) trace_cta(p, 1);
     search_epilogue(p, smem);
 }

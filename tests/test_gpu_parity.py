@@ -492,18 +492,23 @@ def test_long_patterns(path):
     assert ei.value.code == hc.HC_ETOOLONG
 
 
-def test_stream_tma_variant():
-    """The stream path with 1-D TMA bulk copies per chunk (opts.tma_chunk > 0):
-    unaligned texts, edge chunks, 2 and 3 buffers, against brute force."""
+def test_stream_copy_variants():
+    """The stream path's two chunk copies: one 1-D TMA bulk copy per chunk (the default) and
+    16-byte cp.async per lane (opts.tma_chunk < 0): unaligned texts, edge chunks (the first
+    chunk, the last chunks, texts ending inside a 16-byte word), shifts below q (m < 2q),
+    2 and 3 buffers, small chunks (many interior chunks per warp), against brute force."""
     rng = np.random.default_rng(79)
     for n in (1000, 70_001, 1_000_003):
         y = I.gen_text("dna", n, 79 + n % 7)
-        for m, q in [(8, 4), (16, 6), (32, 6), (13, 2)]:
+        for m, q in [(8, 4), (16, 6), (32, 6), (13, 2), (4, 3), (9, 8)]:
             o = int(rng.integers(0, n - m))
             x = y[o:o + m].copy()
             want = oracle.brute(x, y)
             for off in (0, 5, 15):
                 for stages in (2, 3):
-                    got = gpu(hc.prepare(x, q, 12), to_dev(y, off), path=hc.PATH_STREAM,
-                              tma_chunk=16, stages=stages)
-                    assert np.array_equal(got, want), (n, m, off, stages)
+                    for tma, tile, spl in ((0, 0, 0), (-1, 0, 0), (0, 700, 0), (-1, 700, -1), (0, 0, -1)):
+                        # seg_per_lane < 0: final drain on global text instead of private boxes
+                        got = gpu(hc.prepare(x, q, 12), to_dev(y, off), path=hc.PATH_STREAM,
+                                  tma_chunk=tma, stages=stages, tile_bytes=tile,
+                                  max_ctas=3 if tile else 0, seg_per_lane=spl)
+                        assert np.array_equal(got, want), (n, m, off, stages, tma, tile, spl)

@@ -100,7 +100,17 @@ def main():
                   + (f" epilogue ordering {st['dbg'][0] / 1e3:.2f} us for {st['dbg'][1]} positions"
                      if args.debug == 10 else ""),
                   flush=True)
-            if args.trace and r == args.reps - 1 and st["path"] == 2:
+            if args.trace and args.debug == 12:
+                # latest passage of each critical-path point over all warps, us after the
+                # earliest CTA entry
+                g, T = st["grid"], args.trace
+                ts = tr[g * (T * 4 + 2) + 8: g * (T * 4 + 2) + 8 + 9].cpu().numpy().astype("uint64")
+                t0 = int(~ts[0])
+                names = ["entry", "table", "-", "loop done", "q1 drained", "phase B done", "flushed",
+                         "ticket", "published"]
+                print("  path (us after first CTA entry): " + ", ".join(
+                    f"{nm} {(int(t) - t0) / 1e3:.2f}" for nm, t in zip(names[1:], ts[1:]) if int(t)))
+            elif args.trace and r == args.reps - 1 and st["path"] == 2:
                 # gather: per-warp events (trace_tiles >= 8): table loaded, filtered, drained, flushed
                 import numpy as np
                 g, T = st["grid"], args.trace
