@@ -130,7 +130,7 @@ typedef struct hc_search_opts {
                                   grid x trace_tiles x 4 %globaltimer stamps per (CTA, tile)) */
     int trace_tiles;
     int surv_warps;   /* staged: survivor/producer warps per CTA (0 = default) */
-    int block_warps;  /* stream: warps per CTA, 1..8 (0 = default 8) */
+    int block_warps;  /* stream: warps per CTA, 1..24 (0 = default: up to 24, one CTA per SM) */
     int no_multi;     /* hc_search_batch: 1 = no multi-pattern launches (each pattern alone) */
 } hc_search_opts;
 

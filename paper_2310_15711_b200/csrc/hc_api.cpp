@@ -37,9 +37,6 @@ struct hc_handle {
     uint32_t *dF = nullptr;        // device image: F | filter bitmap | x (zero-padded)
     uint32_t *dFbits = nullptr;
     uint8_t *dx = nullptr;
-    uint16_t *dFrank = nullptr;    // ... | rank table | compact F (stream path)
-    uint32_t *dFc = nullptr;
-    uint32_t nfc = 0;              // non-empty words of F
     std::shared_ptr<void> block;   // hc_prepare_batch: device block shared by the batch
 };
 
@@ -91,44 +88,27 @@ void build_table(const uint8_t *x, uint32_t m, uint32_t q, uint32_t alpha, uint3
 
 // Device image of a handle's table, one allocation: F (2^alpha words) | the filter bitmap
 // (bit v set iff F[v] != 0: the l.6 test of Fig. 5 alone, 2^alpha bits, at least 16 B) |
-// x followed by at least 24 zero bytes | the rank table (u16 per bitmap word: non-empty
-// words of F below it) | compact F (the non-empty words of F in order of v; at most
-// min(m, 2^alpha)).  The last two serve the stream path, which keeps the bitmap (one copy
-// per lane), the rank table and compact F in shared memory instead of F: F[v] =
-// bit v ? Fc[rank[v >> 5] + popc(bitmap word below bit v)] : 0.  Each part starts 16-byte
-// aligned and has a size that is a multiple of 16, so the kernels can move F and x with
-// 1-D TMA bulk copies and 16-byte loads without reading past the image.
+// x followed by at least 24 zero bytes.  Each part starts 16-byte aligned and has a
+// size that is a multiple of 16, so the kernels can move F and x with 1-D TMA bulk copies
+// and 16-byte loads without reading past the image.
 struct ImageLayout {
-    size_t f_off, bits_off, x_off, rank_off, fc_off, bytes;
+    size_t f_off, bits_off, x_off, bytes;
 };
 ImageLayout image_layout(uint32_t alpha, size_t m) {
     ImageLayout L;
     const size_t fbytes = (size_t(1) << alpha) * sizeof(uint32_t);
-    const size_t nwords = std::max<size_t>(1, (size_t(1) << alpha) / 32);
-    const size_t nfc = std::min<size_t>(m, size_t(1) << alpha);
     L.f_off = 0;
     L.bits_off = (fbytes + 15) & ~size_t(15);
     L.x_off = L.bits_off + std::max<size_t>(16, ((size_t(1) << alpha) / 8 + 15) & ~size_t(15));
-    L.rank_off = L.x_off + ((m + 24 + 15) & ~size_t(15));
-    L.fc_off = L.rank_off + ((nwords * 2 + 15) & ~size_t(15));
-    L.bytes = L.fc_off + std::max<size_t>(16, (nfc * 4 + 15) & ~size_t(15));
+    L.bytes = L.x_off + ((m + 24 + 15) & ~size_t(15));
     return L;
 }
-void write_image(hc_handle *h, uint8_t *dst) {   // dst: image_layout(...).bytes, zeroed
+void write_image(const hc_handle *h, uint8_t *dst) {   // dst: image_layout(...).bytes, zeroed
     const ImageLayout L = image_layout(h->alpha, h->m);
     std::memcpy(dst + L.f_off, h->F.data(), h->F.size() * sizeof(uint32_t));
     uint32_t *bits = reinterpret_cast<uint32_t *>(dst + L.bits_off);
-    uint16_t *rank = reinterpret_cast<uint16_t *>(dst + L.rank_off);
-    uint32_t *fc = reinterpret_cast<uint32_t *>(dst + L.fc_off);
-    uint32_t cnt = 0;
-    for (size_t v = 0; v < h->F.size(); ++v) {
-        if ((v & 31) == 0) rank[v >> 5] = static_cast<uint16_t>(cnt);
-        if (h->F[v]) {
-            bits[v >> 5] |= 1u << (v & 31);
-            fc[cnt++] = h->F[v];
-        }
-    }
-    h->nfc = cnt;
+    for (size_t v = 0; v < h->F.size(); ++v)
+        if (h->F[v]) bits[v >> 5] |= 1u << (v & 31);
     std::memcpy(dst + L.x_off, h->x.data(), h->m);
 }
 void bind_image(hc_handle *h, uint8_t *base) {
@@ -136,8 +116,6 @@ void bind_image(hc_handle *h, uint8_t *base) {
     h->dF = reinterpret_cast<uint32_t *>(base + L.f_off);
     h->dFbits = reinterpret_cast<uint32_t *>(base + L.bits_off);
     h->dx = base + L.x_off;
-    h->dFrank = reinterpret_cast<uint16_t *>(base + L.rank_off);
-    h->dFc = reinterpret_cast<uint32_t *>(base + L.fc_off);
 }
 
 // Per-host-thread, per-device scratch: [kCtr counter words | positions (cap u32)] plus
@@ -262,7 +240,7 @@ constexpr uint32_t kDefaultStages = 2;
 constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
 constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per warp chunk
 constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
-constexpr uint32_t kDefaultStreamWarps = 8;     // stream path: warps per CTA
+constexpr uint32_t kDefaultStreamWarps = 24;    // stream path: warps per CTA (one CTA per SM)
 constexpr uint32_t kShcLaneBytes = 128;         // SHC path: text bytes per lane and chunk
 // hc_search_batch: patterns of equal (m, q, alpha) with shifts up to this share one
 // streamed pass over the text (multi-pattern stream kernel)
@@ -296,9 +274,6 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
     p.n = nn;
     p.F = h->dF;
     p.Fbits = h->dFbits;
-    p.Frank = h->dFrank;
-    p.Fc = h->dFc;
-    p.nfc = h->nfc;
     p.x = h->dx;
     p.m = m;
     p.q = q;
@@ -365,10 +340,34 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         // chunk bytes [a_k0 - 2q + 1, a_k1 - q] plus 16-byte alignment slack
         p.stage_bytes = (p.seg_per_chunk * S + 2 * q + 32 + 15) & ~15u;
         p.stages = o.stages >= 2 && o.stages <= 4 ? static_cast<uint32_t>(o.stages) : kDefaultStreamBufs;
-        p.block_warps = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps)
-                                                                  : kDefaultStreamWarps;
         // chunks move by one 1-D TMA bulk copy each (tma_chunk < 0: 16-byte cp.async per lane)
         p.tma_chunk = o.tma_chunk < 0 ? 0u : 1u;
+        // One CTA per SM with up to 24 warps: F and the per-lane filter bitmaps (2^alpha words
+        // each) are held once per SM instead of once per 8-warp CTA, which leaves room for
+        // 24 warps' chunk buffers.  Fewer warps when the buffers do not fit; the filter bitmap
+        // unreplicated (lane_bits = 0) when even 8 warps do not fit beside the replicas.
+        p.lane_bits = 1;
+        if (o.block_warps >= 1 && o.block_warps <= 24) {
+            p.block_warps = static_cast<uint32_t>(o.block_warps);
+            if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 1) >
+                smem_budget(h->device))
+                p.lane_bits = 0;
+        } else {
+            p.block_warps = kDefaultStreamWarps;
+            while (p.block_warps > 8 &&
+                   hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 1) >
+                       smem_budget(h->device))
+                p.block_warps -= 4;
+            if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 1) >
+                smem_budget(h->device)) {
+                p.lane_bits = 0;
+                p.block_warps = kDefaultStreamWarps;
+                while (p.block_warps > 8 &&
+                       hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 0) >
+                           smem_budget(h->device))
+                    p.block_warps -= 4;
+            }
+        }
         // final drain on private boxes (hc_stream.cu): 16 bytes of slack + the segment's reach
         // m + S - 1 in whole 16-byte words, one box per lane in the warp's idle chunk buffers
         {
@@ -377,7 +376,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         }
         // shifts too long for per-warp buffers (S > ~200) take the gather path, which
         // reads only the q-grams it hashes anyway
-        if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps) >
+        if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, p.lane_bits) >
             smem_budget(h->device))
             path = HC_PATH_GATHER;
     }
@@ -397,8 +396,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         // box: the lane's bytes (c S + m - 1) in whole 16-byte words, then x (m) and the
         // 8-byte word reads around its end
         p.slot_bytes = (c * S + 2 * m + 40 + 15) & ~15u;
-        uint32_t nw = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps)
-                                                                : kDefaultStreamWarps;
+        uint32_t nw = o.block_warps >= 1 && o.block_warps <= 8 ? static_cast<uint32_t>(o.block_warps) : 8u;
         while (nw > 1 && hc::shc_smem_bytes(p.alpha, m, p.stage_bytes, p.slot_bytes, nw) >
                              smem_budget(h->device))
             --nw;
@@ -914,7 +912,7 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
                 if (path != multi_path) continue;
                 if (stream_multi) {
                     p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
-                                                      : (g > 2 ? 16u : p.block_warps);
+                                                      : (g > 2 ? 16u : 8u);
                     if (p.stages > 3) p.stages = 3;
                 } else {   // gather access, no stage buffers
                     p.mgather = 1;

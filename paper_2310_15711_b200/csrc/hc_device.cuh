@@ -231,52 +231,33 @@ struct FBits {
     }
 };
 
-// Stream path: the filter bitmap replicated per lane in shared memory (word (v >> 5) of
-// lane l's copy at word index (v >> 5) * 32 + l, i.e. in bank l), so the l.6 test of 32
-// random hash values never conflicts (the same lookups in F: ~5 wavefronts per load on
-// DNA, measured 6 us of a 64 us search at m = 16 and 13 us of 88 at m = 8).  Same size as
-// F (2^alpha words), which it replaces in shared memory.  The survivors' F words come
-// from compact F (the <= S non-empty words in order of v) through the rank table:
-// F[v] = bit v ? Fc[rank[v >> 5] + popc(bits of the word below v)] : 0.
-struct LaneBitsF {
-    uint32_t col;          // shared addresses: this lane's bitmap column (table + 4 * lane),
-    uint32_t rank, fc;     // the rank table (u16 per bitmap word) and compact F
+// Stream path, phase A: the filter bitmap replicated per lane in shared memory (word
+// (v >> 5) of lane l's copy at word index (v >> 5) * 32 + l, i.e. in bank l; sh = 7), so the
+// l.6 test of 32 random hash values never conflicts.  (The same lookups in F: ~5
+// wavefronts per load on DNA, measured 6 us of a 64 us search at m = 16 and 13 us of 88 at
+// m = 8.)  The replicas take 2^alpha words, as F does; where they do not fit the kernel
+// keeps one copy (col the same in all lanes, sh = 2).  The survivors read F itself.
+struct PassBits {
+    uint32_t col;          // shared address of this lane's column (table + 4 * lane, or table)
+    uint32_t sh;           // log2 of the byte stride between bitmap words: 7 or 2
     __device__ __forceinline__ bool pass(uint32_t v) const {
-        return (lds32(col + ((v >> 5) << 7)) >> (v & 31)) & 1u;
-    }
-    __device__ __forceinline__ uint32_t operator[](uint32_t v) const {
-        const uint32_t w = lds32(col + ((v >> 5) << 7)), b = v & 31;
-        uint32_t z = 0;
-        if ((w >> b) & 1u) {
-            uint32_t r;
-            asm("ld.shared.u16 %0, [%1];" : "=r"(r) : "r"(rank + 2 * (v >> 5)));
-            z = lds32(fc + 4 * (r + __popc(w & ((1u << b) - 1u))));
-        }
-        return z;
+        return (lds32(col + ((v >> 5) << sh)) >> (v & 31)) & 1u;
     }
 };
-// builds the per-lane copies from the global bitmap (2^alpha bits, >= 4 words), whole CTA
-__device__ __forceinline__ void load_lane_bits(const KParams &p, uint32_t *tab) {
+// builds the bitmap (replicated or not) from the global one (2^alpha bits, >= 4 words);
+// whole CTA, one round trip: every warp loads up to 32 words and hands them round by shuffle
+__device__ __forceinline__ void load_pass_bits(const KParams &p, uint32_t *tab) {
     const uint32_t nw = (1u << p.alpha) > 32 ? (1u << p.alpha) / 32 : 1u;
-    for (uint32_t i0 = threadIdx.x; i0 < nw * 32; i0 += 8 * blockDim.x) {
-        uint32_t v[8];
-#pragma unroll
-        for (uint32_t r = 0; r < 8; ++r) {
-            const uint32_t i = i0 + r * blockDim.x;
-            if (i < nw * 32) v[r] = __ldg(p.Fbits + (i >> 5));
-        }
-#pragma unroll
-        for (uint32_t r = 0; r < 8; ++r) {
-            const uint32_t i = i0 + r * blockDim.x;
-            if (i < nw * 32) tab[i] = v[r];
-        }
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    if (!p.lane_bits) {
+        for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) tab[i] = __ldg(p.Fbits + i);
+        return;
     }
-}
-// the rank table and compact F of the image, into shared memory (whole CTA)
-__device__ __forceinline__ void load_rank_fc(const KParams &p, uint16_t *srank, uint32_t *sfc) {
-    const uint32_t nw = (1u << p.alpha) > 32 ? (1u << p.alpha) / 32 : 1u;
-    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) srank[i] = __ldg(p.Frank + i);
-    for (uint32_t i = threadIdx.x; i < p.nfc; i += blockDim.x) sfc[i] = __ldg(p.Fc + i);
+    for (uint32_t base = warp * 32; base < nw; base += NW * 32) {
+        const uint32_t v = base + lane < nw ? __ldg(p.Fbits + base + lane) : 0u;
+        const uint32_t cnt = min(32u, nw - base);
+        for (uint32_t k = 0; k < cnt; ++k) tab[(base + k) * 32 + lane] = __shfl_sync(HC_FULL, v, k);
+    }
 }
 
 // The 8 text bytes y[p-7 .. p] as a little-endian u64 (byte 7 = y[p]).  Only the
@@ -349,28 +330,15 @@ __device__ __forceinline__ uint32_t qhash(uint64_t W, uint32_t mask) {
 // shared memory, 16-aligned).  8 bytes per step, then a byte tail.
 template <class T>
 __device__ __noinline__ bool verify(const T &t, const uint8_t *sx, uint32_t start, uint32_t m) {
-    // 8-byte words, four loads in flight per round (one memory round trip per 32 bytes, not
-    // one per word); the last m % 8 bytes by an overlapping word (m >= 8) or bytewise
-    uint64_t bad = 0;
-    if (m >= 8 && (m & 7u)) {
-        const uint32_t o = m - 8, sh = 8 * (o & 7u);
-        const uint64_t *w = reinterpret_cast<const uint64_t *>(sx + (o & ~7u));
-        const uint64_t b = shr64(w[0], sh) | shl64(w[1], 64 - sh);   // x[m-8 .. m-1], sh > 0
-        bad = end8<8>(t, start + m - 1) ^ b;
+    uint32_t k = 0;
+    for (; k + 8 <= m; k += 8) {
+        const uint64_t a = end8<8>(t, start + k + 7);
+        const uint64_t b = *reinterpret_cast<const uint64_t *>(sx + k);
+        if (a != b) return false;
     }
-    for (uint32_t k = 0; k + 8 <= m; k += 32) {
-        uint64_t a[4];
-#pragma unroll
-        for (uint32_t r = 0; r < 4; ++r) a[r] = k + 8 * r + 8 <= m ? end8<8>(t, start + k + 8 * r + 7) : 0ull;
-#pragma unroll
-        for (uint32_t r = 0; r < 4; ++r)
-            if (k + 8 * r + 8 <= m) bad |= a[r] ^ *reinterpret_cast<const uint64_t *>(sx + k + 8 * r);
-        if (bad) return false;
-    }
-    if (m < 8)
-        for (uint32_t k = 0; k < m; ++k)
-            if (t.byte(start + k) != sx[k]) return false;
-    return bad == 0;
+    for (; k < m; ++k)
+        if (t.byte(start + k) != sx[k]) return false;
+    return true;
 }
 
 // The same comparison done by the whole warp, 4 x 8 bytes per lane per round.
@@ -1054,25 +1022,19 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
     }
     __syncthreads();
     HC_EPI_TS(3);
-    // exclusive scan of the NB counters: thread t owns NB / T consecutive counters (one or
-    // two 16-byte vectors when NB >= 4 T... else one vector for t < NB / 4)
+    // exclusive scan of the NB counters: thread t < NB / per owns `per` consecutive counters
+    // (a power of two >= 4, read as 16-byte vectors; 4 or 8 for blocks of >= 256 threads)
     {
-        const uint32_t per = NB / T >= 4 ? NB / T : 4u;          // counters per owning thread
+        uint32_t per = 4;
+        while (per * T < NB) per *= 2;
         const uint32_t owners = NB / per;
-        uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         uint32_t loc = 0, big = 0;
         if (t < owners) {
             const uint4 *c4 = reinterpret_cast<const uint4 *>(c + t * per);
-#pragma unroll
-            for (uint32_t u = 0; u < 2; ++u)
-                if (4 * u < per) {
-                    const uint4 x = c4[u];
-                    v[4 * u] = x.x; v[4 * u + 1] = x.y; v[4 * u + 2] = x.z; v[4 * u + 3] = x.w;
-                }
-#pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                big |= v[u] > kEpiBucketMax;
-                loc += v[u];
+            for (uint32_t u = 0; u < per / 4; ++u) {
+                const uint4 x = c4[u];
+                big |= max(max(x.x, x.y), max(x.z, x.w)) > kEpiBucketMax;
+                loc += x.x + x.y + x.z + x.w;
             }
         }
         uint32_t incl = loc;
@@ -1087,16 +1049,15 @@ static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t co
         for (uint32_t w = 0; w < warp; ++w) run += tmp[w];
         if (t < owners) {
             uint4 *c4 = reinterpret_cast<uint4 *>(c + t * per);
-#pragma unroll
-            for (uint32_t u = 0; u < 2; ++u)
-                if (4 * u < per) {
-                    uint4 x;
-                    x.x = run; run += v[4 * u];
-                    x.y = run; run += v[4 * u + 1];
-                    x.z = run; run += v[4 * u + 2];
-                    x.w = run; run += v[4 * u + 3];
-                    c4[u] = x;
-                }
+            for (uint32_t u = 0; u < per / 4; ++u) {
+                const uint4 v = c4[u];
+                uint4 x;
+                x.x = run; run += v.x;
+                x.y = run; run += v.y;
+                x.z = run; run += v.z;
+                x.w = run; run += v.w;
+                c4[u] = x;
+            }
         }
         __syncthreads();
     }

@@ -14,9 +14,6 @@ struct KParams {
     uint32_t n;          // text length (n >= m, n <= HC_MAX_TEXT)
     const uint32_t *F;   // filter table, device, 2^alpha words
     const uint32_t *Fbits;  // filter bitmap, device, 2^alpha bits (bit v = F[v] != 0), >= 16 B
-    const uint16_t *Frank;  // per bitmap word: non-empty words of F below it (stream path)
-    const uint32_t *Fc;     // the nfc non-empty words of F in order of v (stream path)
-    uint32_t nfc;
     const uint8_t *x;    // pattern, device, followed by >= 24 zero bytes (16-byte aligned)
     uint32_t m, q, s, mask, hv;
     uint32_t S;          // shift m - q + 1: also the segment length
@@ -33,6 +30,7 @@ struct KParams {
     uint32_t seg_per_chunk; // segments per warp chunk
     uint32_t nchunks;
     uint32_t block_warps;   // stream / SHC paths: warps per CTA
+    uint32_t lane_bits;     // stream: filter bitmap replicated per lane in shared memory
     uint32_t shc;           // SHC path (chunk geometry: whole segments)
     uint32_t mgather;       // multi-pattern kernel without staging (gather access)
     // output
@@ -116,11 +114,13 @@ int staged_smem_bytes(uint32_t alpha, uint32_t m, uint32_t stage_bytes, uint32_t
 int gather_smem_bytes(uint32_t alpha, uint32_t m);
 int shc_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t box_bytes,
                    uint32_t nwarps);
-int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs, uint32_t nwarps);
+int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs, uint32_t nwarps,
+                      uint32_t lane_bits);
 
 constexpr int kStagedThreads = 256;
 constexpr int kGatherThreads = 256;
-constexpr int kStreamMaxThreads = 256;
+constexpr int kStreamMaxThreads = 256;   // SHC and (x2) multi-pattern kernels
+constexpr int kStreamFatThreads = 768;   // stream kernel: one CTA per SM, up to 24 warps
 constexpr int kWarpBuf = 64;  // per-warp match buffer entries (shared memory)
 
 }  // namespace hc

@@ -20,16 +20,17 @@ namespace hc {
 // buffer; the lattice survivors go through first_steps and phase B on global text
 // (the chunk was just streamed through L2), exactly as on the gather path.
 struct StreamLayout {
-    uint32_t f_off, x_off, rank_off, fc_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
+    uint32_t f_off, bits_off, x_off, q_off, q2_off, wbuf_off, ctr_off, buf_off, total;
 };
 __host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m, uint32_t nwarps,
-                                                      uint32_t buf_bytes, uint32_t bufs) {
+                                                      uint32_t buf_bytes, uint32_t bufs,
+                                                      uint32_t lane_bits) {
     StreamLayout L;
     L.f_off = 0;
-    L.x_off = round_up(max((1u << alpha) * 4u, 128u), 16);   // the per-lane filter bitmaps
-    L.rank_off = L.x_off + round_up(m + 8, 16);
-    L.fc_off = L.rank_off + round_up(2u * max((1u << alpha) / 32u, 1u), 16);
-    L.q_off = L.fc_off + round_up(4u * min(m, 1u << alpha), 16);
+    L.bits_off = round_up((1u << alpha) * 4u, 16);
+    // the filter bitmap: one copy per lane (2^alpha words, at least one word each) or one copy
+    L.x_off = L.bits_off + (lane_bits ? max((1u << alpha) * 4u, 128u) : max((1u << alpha) / 8u, 16u));
+    L.q_off = L.x_off + round_up(m + 8, 16);
     L.q2_off = L.q_off + nwarps * kStreamQ1 * 4u;
     L.wbuf_off = L.q2_off + nwarps * kWarpBuf * 4u;
     L.ctr_off = L.wbuf_off + nwarps * kWarpBuf * 4u;
@@ -39,8 +40,8 @@ __host__ __device__ inline StreamLayout stream_layout(uint32_t alpha, uint32_t m
     return L;
 }
 int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t bufs,
-                      uint32_t nwarps) {
-    return static_cast<int>(stream_layout(alpha, m, nwarps, buf_bytes, bufs).total);
+                      uint32_t nwarps, uint32_t lane_bits) {
+    return static_cast<int>(stream_layout(alpha, m, nwarps, buf_bytes, bufs, lane_bits).total);
 }
 
 // Phase A of the stream path over lattice points [k0, k1) of a staged chunk: the same
@@ -56,7 +57,7 @@ struct StreamQueue {
     // first steps of 32 queued survivors, on the chunk's stage (the queue only ever
     // holds survivors of the chunk being filtered: it is drained at the chunk's end)
     template <class TT>
-    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
+    __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
                                             const TT &txt, uint32_t lane) {
         __syncwarp();
         const uint32_t e = q1[n1 - 32 + lane];
@@ -67,7 +68,7 @@ struct StreamQueue {
         sink.steps_e_on(txt, true, e);
     }
     template <class TT>
-    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
+    __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
                                               const TT &txt, uint32_t lane) {
         while (n1 >= 32) drain32(sink, txt, lane);
         if (n1) {
@@ -84,10 +85,10 @@ struct StreamQueue {
 };
 
 template <int Q, int SH>
-__device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &txt, const LaneBitsF &sF,
+__device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &txt, const PassBits &sF,
                                               uint32_t k0, uint32_t k1, uint32_t lane,
                                               StreamQueue<Q, SH> &qu,
-                                              WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink) {
+                                              WarpQueueSink<Q, SH, GlobalText, FTable> &sink) {
     const uint32_t step = 32 * p.S;
     uint32_t pos = p.m - 1 + (k0 + lane) * p.S;   // window end a_k of lattice point k0 + lane
     uint32_t k = k0;
@@ -159,8 +160,8 @@ __device__ __forceinline__ void stream_prologue(const KParams &p, uint32_t bufs0
         stream_issue(p, gw + b * total_warps, bufs0 + b * p.stage_bytes, lane);
 }
 template <int Q, int SH, int NB>
-__device__ __forceinline__ void stream_loop(const KParams &p, const LaneBitsF &sF,
-                                            WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
+__device__ __forceinline__ void stream_loop(const KParams &p, const PassBits &sF,
+                                            WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
                                             StreamQueue<Q, SH> &qu, uint32_t bufs0,
                                             uint32_t gw, uint32_t total_warps, uint32_t lane) {
     const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
@@ -255,8 +256,8 @@ __device__ __forceinline__ void stream_prologue_tma(const KParams &p, const TmaS
     }
 }
 template <int Q, int SH, int NB>
-__device__ __forceinline__ void stream_loop_tma(const KParams &p, const LaneBitsF &sF,
-                                                WarpQueueSink<Q, SH, GlobalText, LaneBitsF> &sink,
+__device__ __forceinline__ void stream_loop_tma(const KParams &p, const PassBits &sF,
+                                                WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
                                                 StreamQueue<Q, SH> &qu, const TmaStream &ts,
                                                 uint32_t gw, uint32_t total_warps, uint32_t lane) {
     const uint32_t stride = total_warps * ts.D;
@@ -299,7 +300,7 @@ __device__ __forceinline__ void stream_loop_tma(const KParams &p, const LaneBits
 // shared-memory latency.  A lattice survivor starts at its window end a_k (first_steps is
 // only a shortcut of the same loop).  p.slot_bytes = box size (0: boxes do not fit).
 template <int Q, int SH>
-__device__ __forceinline__ void final_drain_boxes(const KParams &p, const LaneBitsF &sF, const uint8_t *sx,
+__device__ __forceinline__ void final_drain_boxes(const KParams &p, const FTable &sF, const uint8_t *sx,
                                                   const uint32_t *q1, uint32_t n1, const uint32_t *q2,
                                                   uint32_t n2, uint32_t boxes, WarpOut &wo, uint32_t lane) {
     const uintptr_t y = reinterpret_cast<uintptr_t>(p.y), ye = y + p.n;
@@ -340,12 +341,12 @@ template <int Q, int SH>
 #ifndef HC_STREAM_MINB
 #define HC_STREAM_MINB 3
 #endif
-// 3 CTAs per SM at most (shared memory allows 2-3): up to 85 registers, no spills in the
-// filter loop (at 64 the loop spilled ~600 B per thread)
-__global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kernel(const KParams p) {
+// One CTA of up to 24 warps per SM (F and the per-lane filter bitmaps are held once per SM):
+// up to 85 registers, no spills in the filter loop (at 64 the loop spilled ~600 B per thread)
+__global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t NW = blockDim.x / 32;
-    const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages);
+    const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages, p.lane_bits);
     uint32_t *sFp = reinterpret_cast<uint32_t *>(smem + L.f_off);
     uint8_t *sx = smem + L.x_off;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -367,18 +368,17 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
     } else if (p.stages == 2) stream_prologue<2>(p, bufs0, gw, total_warps, lane);
     else if (p.stages == 3) stream_prologue<3>(p, bufs0, gw, total_warps, lane);
     else stream_prologue<4>(p, bufs0, gw, total_warps, lane);
-    load_lane_bits(p, sFp);
-    load_rank_fc(p, reinterpret_cast<uint16_t *>(smem + L.rank_off),
-                 reinterpret_cast<uint32_t *>(smem + L.fc_off));
-    load_x(p, sx);
+    load_pass_bits(p, reinterpret_cast<uint32_t *>(smem + L.bits_off));
+    load_table(p, sFp, sx);
     if (tid == 0) s_params[0] = p;
     __syncthreads();
     path_ts(p, 1);
-    const LaneBitsF sF{fence_value(smem_u32(sFp)) + 4 * lane, smem_u32(smem + L.rank_off),
-                       smem_u32(smem + L.fc_off)};
+    const FTable sF{fence_value(smem_u32(sFp))};
+    const PassBits pb{fence_value(smem_u32(smem + L.bits_off)) + (p.lane_bits ? 4 * lane : 0u),
+                      p.lane_bits ? 7u : 2u};
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
     const GlobalText gtxt{p.y};
-    WarpQueueSink<Q, SH, GlobalText, LaneBitsF> sink{p, gtxt, sF, sx, nullptr,
+    WarpQueueSink<Q, SH, GlobalText, FTable> sink{p, gtxt, sF, sx, nullptr,
                                           reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
                                           0u, 0u, wo, lane};
     uint32_t *ctr = reinterpret_cast<uint32_t *>(smem + L.ctr_off) + warp;
@@ -387,17 +387,17 @@ __global__ void __launch_bounds__(kStreamMaxThreads, HC_STREAM_MINB) stream_kern
     StreamQueue<Q, SH> qu{reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kStreamQ1, ctr, 0u};
     if (p.tma_chunk) {
         if (p.stages == 4)
-            stream_loop_tma<Q, SH, 4>(p, sF, sink, qu, ts, gw, total_warps, lane);
+            stream_loop_tma<Q, SH, 4>(p, pb, sink, qu, ts, gw, total_warps, lane);
         else if (p.stages == 3)
-            stream_loop_tma<Q, SH, 3>(p, sF, sink, qu, ts, gw, total_warps, lane);
+            stream_loop_tma<Q, SH, 3>(p, pb, sink, qu, ts, gw, total_warps, lane);
         else
-            stream_loop_tma<Q, SH, 2>(p, sF, sink, qu, ts, gw, total_warps, lane);
+            stream_loop_tma<Q, SH, 2>(p, pb, sink, qu, ts, gw, total_warps, lane);
     } else if (p.stages == 2)
-        stream_loop<Q, SH, 2>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+        stream_loop<Q, SH, 2>(p, pb, sink, qu, bufs0, gw, total_warps, lane);
     else if (p.stages == 3)
-        stream_loop<Q, SH, 3>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+        stream_loop<Q, SH, 3>(p, pb, sink, qu, bufs0, gw, total_warps, lane);
     else
-        stream_loop<Q, SH, 4>(p, sF, sink, qu, bufs0, gw, total_warps, lane);
+        stream_loop<Q, SH, 4>(p, pb, sink, qu, bufs0, gw, total_warps, lane);
     path_ts(p, 3);
     if (p.slot_bytes) {
         __syncwarp();
@@ -435,7 +435,7 @@ cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int c
     KernFn kern = pick<PickStream>(p.q, p.s);
     if (!kern) return cudaErrorInvalidValue;
     const uint32_t nw = p.block_warps;
-    const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, nw);
+    const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, nw, p.lane_bits);
     const long ctas = (p.nchunks + nw - 1) / nw;
     KParams a = p;
     a.epi_cap = epi_cap_for(smem);

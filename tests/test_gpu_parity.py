@@ -512,3 +512,19 @@ def test_stream_copy_variants():
                                   tma_chunk=tma, stages=stages, tile_bytes=tile,
                                   max_ctas=3 if tile else 0, seg_per_lane=spl)
                         assert np.array_equal(got, want), (n, m, off, stages, tma, tile, spl)
+
+
+def test_epilogue_ordering_any_block_size():
+    """The fused epilogue orders up to 8,192 positions in the last CTA, whatever its size:
+    stream CTAs of 1..24 warps (the default is one 24-warp CTA per SM; fewer warps when
+    alpha is large), counts from a few hundred (bucket pass) to just below and above the
+    epilogue's capacity (host ordering)."""
+    rng = np.random.default_rng(97)
+    for n, m in ((40_000, 3), (200_000, 3), (450_000, 3), (700_000, 3)):
+        y = rng.integers(0, 4, n, dtype=np.uint8)
+        x = y[77:77 + m].copy()
+        want = oracle.brute(x, y)
+        for bw in (1, 3, 5, 8, 12, 20, 24):
+            for alpha in (8, 12):
+                got = gpu(hc.prepare(x, 2, alpha), to_dev(y, 3), path=hc.PATH_STREAM, block_warps=bw)
+                assert np.array_equal(got, want), (n, bw, alpha, len(got), len(want))
