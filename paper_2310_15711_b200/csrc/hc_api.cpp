@@ -768,12 +768,9 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         if (o.debug == 10) {
             unsigned long long ts[16] = {};
             hc::read_epi_ts(ts);
-            std::fprintf(stderr, "epilogue block_order phases (ns): load %llu minmax %llu hist %llu "
-                                 "scan %llu scatter %llu rank %llu\n", ts[1] - ts[0], ts[2] - ts[1],
-                         ts[3] - ts[2], ts[4] - ts[3], ts[5] - ts[4], ts[6] - ts[5]);
-            std::fprintf(stderr, "epilogue block_order phases (cycles): load %llu minmax %llu hist %llu "
-                                 "scan %llu scatter %llu rank %llu\n", ts[9] - ts[8], ts[10] - ts[9],
-                         ts[11] - ts[10], ts[12] - ts[11], ts[13] - ts[12], ts[14] - ts[13]);
+            std::fprintf(stderr, "epilogue block_order phases (ns): load %llu hist %llu scan %llu "
+                                 "scatter %llu rank+store %llu\n", ts[1] - ts[0], ts[3] - ts[1],
+                         ts[4] - ts[3], ts[5] - ts[4], ts[6] - ts[5]);
         }
 #endif
         if (HC_INSTRUMENT && (o.debug == 5 || o.debug == 10) && stats) {

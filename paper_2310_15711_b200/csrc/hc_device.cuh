@@ -135,6 +135,11 @@ __device__ __forceinline__ void path_ts(const KParams &p, uint32_t i) {
         atomicMax(a, i == 0 ? ~t : t);
     }
 }
+// debug 12: event counters next to the stamps (one lane per warp counts)
+__device__ __forceinline__ void path_cnt(const KParams &p, uint32_t i, uint32_t lane) {
+    if (kInstrument && p.trace && p.debug == 12 && lane == 0)
+        atomicAdd(p.trace + static_cast<size_t>(gridDim.x) * (p.trace_tiles * 4 + 2) + 24 + i, 1ull);
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -492,9 +497,11 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
     // (cheap) lattice filter and first steps, and the host re-runs it on the scan path,
     // which hashes every q-gram once (hc_scan.cu).  Only batches with warp-wide walks (rare
     // on non-repetitive text) read the flag.
-    uint32_t nwalks = 0;
+    uint32_t nwalks = 0, nit = 0;
     while (__any_sync(HC_FULL, active)) {
         if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 4, 1u);
+        path_cnt(p, 0, lane);
+        path_ts(p, 9 + min(nit++, 6u));
         bool need_v = false, stepped = false;
         if (long_walks) {
             // walks that passed kLongWalk link tests and still have >= kLongWalk steps to
@@ -517,6 +524,7 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
                 const uint32_t zL = __shfl_sync(HC_FULL, z, L);
                 uint32_t vL = 0;
                 bool broke = false;
+                path_cnt(p, 1, lane);
                 walk_warp<Q, SH>(p, txt.shfl(L), sF, lane, jL, iL, zL, vL, broke);
                 if (lane == L) {
                     stepped = true;
@@ -596,6 +604,7 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
                 const uint32_t L = __ffs(vm) - 1;
                 vm &= vm - 1;
                 const uint32_t st = __shfl_sync(HC_FULL, e + 1 - p.m, L);
+                path_cnt(p, 2, lane);
                 const bool ok = verify_warp(txt.shfl(L), sx, st, p.m, lane);
                 if (lane == L) found = ok;
             }
@@ -935,16 +944,17 @@ __device__ __forceinline__ void stream_issue(const KParams &p, uint32_t c, uint3
 // own (now idle) shared memory.  One kernel launch per hc_search in the common case;
 // the host orders only what the epilogue could not (hc_finish.cu).
 
-// Orders `count` distinct positions pos[0..count) (2 <= count) into dst[0..k) ascending,
-// in shared memory `sm` (>= epi_bytes(count) bytes), by the whole block.  Small sets by
-// rank counting; larger ones by a bucket pass on the positions' offset from their
-// minimum (power-of-two buckets, count/2 to count of them, at most 2048) and rank
-// counting inside each bucket.  Keys are read as 16-byte vectors, each pass over them
-// is a straight loop of independent shared-memory operations, the counter scan works
-// on 16-byte vectors with warp shuffles, and the sorted keys leave through coalesced
-// 8-byte stores.  Returns false when some bucket holds more than kEpiBucketMax keys
-// (strongly clustered positions): the host then orders them (nothing is assumed of
-// dst).
+// Orders `count` distinct positions pos[0..count) (2 <= count), all < 2^nbits, into
+// dst[0..k) ascending, in shared memory `sm` (>= epi_bytes(count) bytes), by the whole
+// block (any size).  Small sets by rank counting; larger ones by a bucket pass (power-of-two
+// buckets, count/2 to count of them, at most 2048: bucket = position >> sh over the whole
+// text) and rank counting inside each bucket.  When some bucket holds more than
+// kEpiBucketMax keys (clustered positions) the pass is repeated once on the positions'
+// offset from their minimum; false when that does not help either (the host then orders
+// them; nothing is assumed of dst).  The code is kept SMALL (scalar loops, not unrolled):
+// it runs once per search on one SM whose instruction cache has never seen it, and the
+// vectorised version of round 2a spent most of its 12.7 us (4,144 positions) fetching
+// instructions: each phase took 2-3 us however few keys a thread had.
 #if HC_INSTRUMENT
 static __device__ unsigned long long g_epi_ts[16];  // debug 10: block_order phase stamps
 #define HC_EPI_TS(i) do { if (threadIdx.x == 0) { g_epi_ts[i] = gtimer(); g_epi_ts[8 + i] = clock64(); } } while (0)
@@ -954,134 +964,121 @@ static __device__ unsigned long long g_epi_ts[16];  // debug 10: block_order pha
 constexpr uint32_t kEpiRankMax = 256;
 constexpr uint32_t kEpiBucketMax = 64;
 static __device__ __noinline__ bool block_order(const uint32_t *pos, uint32_t count, int64_t *dst, uint32_t k,
-                                                uint8_t *sm) {
-    const uint32_t T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, NWp = T >> 5;
+                                                uint8_t *sm, uint32_t nbits) {
+    const uint32_t T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     uint32_t *tmp = reinterpret_cast<uint32_t *>(sm);            // 64 words
     uint32_t *ks = tmp + 64;                                     // keys, then the sorted keys
     const uint32_t cnt4 = (count + 3) & ~3u;
     // all keys to shared memory with 16-byte cp.async copies: one L2 round trip (the
     // scratch is 16-byte aligned and has >= 3 words of slack past any count)
+#pragma unroll 1
     for (uint32_t i = 4 * t; i < count; i += 4 * T)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(ks + i)), "l"(pos + i)
                      : "memory");
     HC_EPI_TS(0);
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    for (uint32_t i = count + t; i < cnt4; i += T) ks[i] = 0xffffffffu;   // pad the last vector
-    __syncthreads();
     HC_EPI_TS(1);
     if (count <= kEpiRankMax) {
         if (t < count) {
             const uint32_t key = ks[t];
             uint32_t r = 0;
-#pragma unroll 8
+#pragma unroll 1
             for (uint32_t j = 0; j < count; ++j) r += ks[j] < key;
             if (r < k) dst[r] = static_cast<int64_t>(key);
         }
         return true;
     }
-    uint32_t NB = 32;
-    while (NB < 2048 && 2 * NB < count) NB <<= 1;                // count/2 <= NB < count
+    uint32_t NB = 32, lb = 5;
+    while (NB < 2048 && 2 * NB < count) NB <<= 1, ++lb;          // count/2 <= NB < count
     uint32_t *c = ks + cnt4;                                     // NB bucket counters
     uint32_t *k2 = c + NB;                                       // keys grouped by bucket
-    const uint4 *ks4 = reinterpret_cast<const uint4 *>(ks);
-    const uint32_t n4 = cnt4 / 4;
-    // minimum and maximum (the pads are all-ones: excluded from the maximum)
-    uint32_t lo = 0xffffffffu, hi = 0;
-    for (uint32_t i = t; i < n4; i += T) {
-        const uint4 v = ks4[i];
-        lo = min(min(lo, v.x), min(v.y, min(v.z, v.w)));
-        hi = max(max(hi, v.x != 0xffffffffu ? v.x : 0u),
-                 max(v.y != 0xffffffffu ? v.y : 0u,
-                     max(v.z != 0xffffffffu ? v.z : 0u, v.w != 0xffffffffu ? v.w : 0u)));
-    }
-    lo = __reduce_min_sync(HC_FULL, lo);
-    hi = __reduce_max_sync(HC_FULL, hi);
-    if (lane == 0) {
-        tmp[warp] = lo;
-        tmp[32 + warp] = hi;
-    }
-    for (uint32_t i = t; i < NB / 4; i += T) reinterpret_cast<uint4 *>(c)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    lo = tmp[0];
-    hi = tmp[32];
-    for (uint32_t w = 1; w < NWp; ++w) {
-        lo = min(lo, tmp[w]);
-        hi = max(hi, tmp[32 + w]);
-    }
-    uint32_t sh = 0;                                             // (hi - lo) >> sh < NB
-    while (((hi - lo) >> sh) >= NB) ++sh;
-    HC_EPI_TS(2);
-    for (uint32_t i = t; i < n4; i += T) {                       // histogram
-        const uint4 v = ks4[i];
-        const uint32_t base = 4 * i;
-        if (base + 0 < count) atomicAdd(&c[(v.x - lo) >> sh], 1u);
-        if (base + 1 < count) atomicAdd(&c[(v.y - lo) >> sh], 1u);
-        if (base + 2 < count) atomicAdd(&c[(v.z - lo) >> sh], 1u);
-        if (base + 3 < count) atomicAdd(&c[(v.w - lo) >> sh], 1u);
-    }
-    __syncthreads();
-    HC_EPI_TS(3);
-    // exclusive scan of the NB counters: thread t < NB / per owns `per` consecutive counters
-    // (a power of two >= 4, read as 16-byte vectors; 4 or 8 for blocks of >= 256 threads)
-    {
-        uint32_t per = 4;
-        while (per * T < NB) per *= 2;
-        const uint32_t owners = NB / per;
-        uint32_t loc = 0, big = 0;
-        if (t < owners) {
-            const uint4 *c4 = reinterpret_cast<const uint4 *>(c + t * per);
-            for (uint32_t u = 0; u < per / 4; ++u) {
-                const uint4 x = c4[u];
-                big |= max(max(x.x, x.y), max(x.z, x.w)) > kEpiBucketMax;
-                loc += x.x + x.y + x.z + x.w;
-            }
+    uint32_t lo = 0, sh = nbits > lb ? nbits - lb : 0u;          // bucket = (key - lo) >> sh < NB
+    const uint32_t per = (NB + T - 1) / T;                       // counters per scanning thread
+    const uint32_t b0 = min(t * per, NB), b1 = min(b0 + per, NB);
+#pragma unroll 1
+    for (uint32_t attempt = 0;; ++attempt) {
+#pragma unroll 1
+        for (uint32_t i = t; i < NB; i += T) c[i] = 0;
+        __syncthreads();
+#pragma unroll 1
+        for (uint32_t i = t; i < count; i += T) atomicAdd(&c[(ks[i] - lo) >> sh], 1u);   // histogram
+        __syncthreads();
+        HC_EPI_TS(3);
+        uint32_t loc = 0, big = 0;                               // exclusive scan of the counters
+#pragma unroll 1
+        for (uint32_t i = b0; i < b1; ++i) {
+            const uint32_t v = c[i];
+            big |= v > kEpiBucketMax;
+            loc += v;
         }
         uint32_t incl = loc;
-#pragma unroll
+#pragma unroll 1
         for (uint32_t o = 1; o < 32; o <<= 1) {
             const uint32_t x = __shfl_up_sync(HC_FULL, incl, o);
             if (lane >= o) incl += x;
         }
         if (lane == 31) tmp[warp] = incl;
-        if (__syncthreads_or(big)) return false;
-        uint32_t run = incl - loc;
-        for (uint32_t w = 0; w < warp; ++w) run += tmp[w];
-        if (t < owners) {
-            uint4 *c4 = reinterpret_cast<uint4 *>(c + t * per);
-            for (uint32_t u = 0; u < per / 4; ++u) {
-                const uint4 v = c4[u];
-                uint4 x;
-                x.x = run; run += v.x;
-                x.y = run; run += v.y;
-                x.z = run; run += v.z;
-                x.w = run; run += v.w;
-                c4[u] = x;
+        if (!__syncthreads_or(big)) {
+            uint32_t run = incl - loc;
+#pragma unroll 1
+            for (uint32_t w = 0; w < warp; ++w) run += tmp[w];
+#pragma unroll 1
+            for (uint32_t i = b0; i < b1; ++i) {
+                const uint32_t v = c[i];
+                c[i] = run;
+                run += v;
             }
+            break;
+        }
+        if (attempt) return false;
+        // clustered positions: buckets over [min, max] instead of the whole text
+        uint32_t mn = 0xffffffffu, mx = 0;
+#pragma unroll 1
+        for (uint32_t i = t; i < count; i += T) {
+            mn = min(mn, ks[i]);
+            mx = max(mx, ks[i]);
+        }
+        mn = __reduce_min_sync(HC_FULL, mn);
+        mx = __reduce_max_sync(HC_FULL, mx);
+        __syncthreads();                                         // tmp is free again
+        if (lane == 0) {
+            tmp[warp] = mn;
+            tmp[32 + warp] = mx;
         }
         __syncthreads();
+#pragma unroll 1
+        for (uint32_t w = 0; w < (T >> 5); ++w) {
+            mn = min(mn, tmp[w]);
+            mx = max(mx, tmp[32 + w]);
+        }
+        lo = mn;
+        sh = 0;
+        while (((mx - lo) >> sh) >= NB) ++sh;
+        __syncthreads();
     }
+    __syncthreads();
     HC_EPI_TS(4);
-    for (uint32_t i = t; i < n4; i += T) {                       // scatter by bucket
-        const uint4 v = ks4[i];
-        const uint32_t base = 4 * i;
-        if (base + 0 < count) k2[atomicAdd(&c[(v.x - lo) >> sh], 1u)] = v.x;
-        if (base + 1 < count) k2[atomicAdd(&c[(v.y - lo) >> sh], 1u)] = v.y;
-        if (base + 2 < count) k2[atomicAdd(&c[(v.z - lo) >> sh], 1u)] = v.z;
-        if (base + 3 < count) k2[atomicAdd(&c[(v.w - lo) >> sh], 1u)] = v.w;
+#pragma unroll 1
+    for (uint32_t i = t; i < count; i += T) {                    // scatter by bucket
+        const uint32_t key = ks[i];
+        k2[atomicAdd(&c[(key - lo) >> sh], 1u)] = key;
     }
     __syncthreads();                                             // c[b] = end of bucket b
     HC_EPI_TS(5);
+#pragma unroll 1
     for (uint32_t i = t; i < count; i += T) {                    // rank inside the bucket
         const uint32_t key = k2[i];
         const uint32_t b = (key - lo) >> sh;
         const uint32_t b_lo = b ? c[b - 1] : 0u, b_hi = c[b];
         uint32_t r = b_lo;
+#pragma unroll 1
         for (uint32_t j = b_lo; j < b_hi; ++j) r += k2[j] < key;
         ks[r] = key;                                             // sorted (ks is free now)
     }
     __syncthreads();
     const uint32_t kk = min(k, count);
+#pragma unroll 1
     for (uint32_t i = t; i < kk; i += T) dst[i] = static_cast<int64_t>(ks[i]);   // coalesced
     HC_EPI_TS(6);
     return true;
@@ -1105,7 +1102,8 @@ __device__ __forceinline__ bool cta_is_last(uint32_t *ticket) {
 // `smem` is the CTA's dynamic shared memory (idle by now), `smem_bytes` its size.
 __device__ __forceinline__ void publish_search(uint32_t *counter, const uint32_t *out, uint32_t cap,
                                                uint32_t *host_count, int64_t *dst, uint32_t k_out,
-                                               uint32_t epi_cap, uint8_t *smem, bool fault) {
+                                               uint32_t epi_cap, uint8_t *smem, bool fault,
+                                               uint32_t nbits) {
     const uint32_t count = *reinterpret_cast<volatile uint32_t *>(counter);
     bool ordered = count == 0 || dst == nullptr || k_out == 0;
     if (!ordered && count <= cap && count <= epi_cap) {
@@ -1115,7 +1113,7 @@ __device__ __forceinline__ void publish_search(uint32_t *counter, const uint32_t
         } else {
             unsigned long long t0 = 0;
             if (kInstrument && threadIdx.x == 0) t0 = gtimer();
-            ordered = block_order(out, count, dst, k_out, smem);
+            ordered = block_order(out, count, dst, k_out, smem, nbits);
             if (kInstrument && threadIdx.x == 0) {   // debug 10: ordering time, ns
                 counter[6] = static_cast<uint32_t>(gtimer() - t0);
                 counter[7] = count;
@@ -1159,7 +1157,7 @@ __device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem)
         return;
     }
     publish_search(p.counter, p.out, p.cap, p.host_count, p.dst, p.k_out, p.epi_cap, smem,
-                   p.debug == 9);
+                   p.debug == 9, p.nbits);
     __syncthreads();
     if (threadIdx.x == 0) p.counter[2] = 0;
     path_ts(p, 8);

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
     if (cta_is_last(mp.counter[0] + 2)) {
         for (uint32_t i = 0; i < P; ++i) {
             publish_search(mp.counter[i], mp.out[i], mp.cap[i], mp.host_count[i], mp.dst[i],
-                           mp.k_out[i], p.epi_cap, smem, p.debug == 9);
+                           mp.k_out[i], p.epi_cap, smem, p.debug == 9, p.nbits);
             __syncthreads();
         }
         if (tid == 0) mp.counter[0][2] = 0;

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--per-m", type=int, default=4)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--count-only", action="store_true")
+    ap.add_argument("--b-spl", type=int, default=0, help="opts.seg_per_lane for library B")
     args = ap.parse_args()
     libs = [load(os.path.abspath(p)) for p in args.libs]
     cfg = I.CONFIGS[args.config]
@@ -49,6 +50,7 @@ def main():
     sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     st = hc.Stats()
     opts = hc.Opts(time_kernel=1)
+    opts_b = hc.Opts(time_kernel=1, seg_per_lane=args.b_spl)
     tot = [0.0, 0.0]
     for m in args.m or cfg.ms:
         q, a = cfg.qa[m]
@@ -63,7 +65,7 @@ def main():
                     c = libs[k].hc_search_ex(hs[k][i], C.c_void_p(y.data_ptr()), n,
                                              None if args.count_only else C.c_void_p(pos.data_ptr()),
                                              0 if args.count_only else pos.numel(), sp,
-                                             C.byref(opts), C.byref(st))
+                                             C.byref(opts_b if k else opts), C.byref(st))
                     assert c >= 0
                     if cnt[k] is None:
                         cnt[k] = c

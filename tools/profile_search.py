@@ -104,10 +104,12 @@ def main():
                 # latest passage of each critical-path point over all warps, us after the
                 # earliest CTA entry
                 g, T = st["grid"], args.trace
-                ts = tr[g * (T * 4 + 2) + 8: g * (T * 4 + 2) + 8 + 9].cpu().numpy().astype("uint64")
+                ts = tr[g * (T * 4 + 2) + 8: g * (T * 4 + 2) + 8 + 16].cpu().numpy().astype("uint64")
+                cn = tr[g * (T * 4 + 2) + 24: g * (T * 4 + 2) + 24 + 4].cpu().numpy()
+                print(f"  phase B: iterations {cn[0]}, warp-wide walks {cn[1]}, warp-wide verifications {cn[2]}")
                 t0 = int(~ts[0])
                 names = ["entry", "table", "-", "loop done", "q1 drained", "phase B done", "flushed",
-                         "ticket", "published"]
+                         "ticket", "published"] + [f"B it{k}" for k in range(7)]
                 print("  path (us after first CTA entry): " + ", ".join(
                     f"{nm} {(int(t) - t0) / 1e3:.2f}" for nm, t in zip(names[1:], ts[1:]) if int(t)))
             elif args.trace and r == args.reps - 1 and st["path"] == 2:
