@@ -111,7 +111,8 @@ typedef struct hc_search_opts {
     int path;         /* hc_path */
     int tile_bytes;   /* staged: text bytes per shared-memory stage; stream: target text bytes
                          per warp chunk (0 = default) */
-    int stages;       /* staged: TMA pipeline depth; stream: buffers per warp, 2..4 (0 = default 2) */
+    int stages;       /* staged: TMA pipeline depth; multi-pattern stream launches: buffers per
+                         warp, 2 or 3 (the single-pattern stream kernel always uses 2) */
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default);
                          stream: < 0 = final drain on global text (no private boxes) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */
@@ -124,8 +125,7 @@ typedef struct hc_search_opts {
                          valid) exist only in the instrumented build libhc_instr.so
                          (HC_INSTRUMENT=1, tools/); this library returns HC_EINVAL if set */
     int tma_chunk;    /* staged: bytes per TMA bulk copy (0 = one copy per tile stage);
-                         stream: < 0 = chunks by 16-byte cp.async per lane instead of one
-                         1-D TMA bulk copy per chunk (the default) */
+                         (the stream path always moves a chunk by one 1-D TMA bulk copy) */
     unsigned long long *trace; /* must be NULL (instrumented build only: DEVICE buffer of
                                   grid x trace_tiles x 4 %globaltimer stamps per (CTA, tile)) */
     int trace_tiles;

@@ -339,9 +339,8 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         p.nchunks = (K + p.seg_per_chunk - 1) / p.seg_per_chunk;
         // chunk bytes [a_k0 - 2q + 1, a_k1 - q] plus 16-byte alignment slack
         p.stage_bytes = (p.seg_per_chunk * S + 2 * q + 32 + 15) & ~15u;
-        p.stages = o.stages >= 2 && o.stages <= 4 ? static_cast<uint32_t>(o.stages) : kDefaultStreamBufs;
-        // chunks move by one 1-D TMA bulk copy each (tma_chunk < 0: 16-byte cp.async per lane)
-        p.tma_chunk = o.tma_chunk < 0 ? 0u : 1u;
+        p.stages = kDefaultStreamBufs;   // 2 buffers per warp (3 and 4 measured slower)
+        p.tma_chunk = 1;   // chunks move by one 1-D TMA bulk copy each
         // One CTA per SM with up to 24 warps: F and the per-lane filter bitmaps (2^alpha words
         // each) are held once per SM instead of once per 8-warp CTA, which leaves room for
         // 24 warps' chunk buffers.  Fewer warps when the buffers do not fit; the filter bitmap
@@ -910,7 +909,7 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
                 if (stream_multi) {
                     p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
                                                       : (g > 2 ? 16u : 8u);
-                    if (p.stages > 3) p.stages = 3;
+                    p.stages = o.stages == 3 ? 3u : 2u;   // multi-pattern kernel: 2 or 3 buffers
                 } else {   // gather access, no stage buffers
                     p.mgather = 1;
                     p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))

@@ -739,6 +739,9 @@ struct WarpQueueSink {
         steps_e(act, act ? q1[lane] : 0u);
     }
     // first steps of the lattice survivor a_k = e of each active lane -> q2
+    // (An out-of-line copy of the first steps shared by all call sites was measured: the
+    // gather kernel at m >= 512 4-15% faster (smaller code, everything runs cold there), but
+    // m = 64 and the stream kernel's filter loop 5-7% slower: a call inside the hot loop.)
     __device__ __forceinline__ void steps_e(bool act, uint32_t e) { steps_e_on(txt, act, e); }
     // the same, reading the first steps' q-grams from `t2` (e.g. a shared-memory stage)
     template <class T2>

@@ -1,21 +1,15 @@
-// hc_stream.cu — stream path (HC_PATH_STREAM, the default for shifts S <= 32):
-// per-warp chunks staged in shared memory by 16-byte cp.async copies (or one 1-D TMA
-// bulk copy per chunk, opts.tma_chunk), lattice filter on the stage, survivors through
-// first steps on the stage and phase B on global text.  DESIGN.md 5.
+// hc_stream.cu — stream path (HC_PATH_STREAM, the default for shifts S <= 32): one CTA of
+// up to 24 warps per SM; per-warp chunks staged in shared memory by one 1-D TMA bulk copy
+// each; lattice filter on the stage against per-lane copies of the filter bitmap; survivors
+// through first steps and phase B on global text; final drain on private boxes.  DESIGN.md 5.
 #include "hc_device.cuh"
-
-#ifndef HC_STREAM_GLOBAL_FS
-#define HC_STREAM_GLOBAL_FS 1   // first steps on global text (L2), the queue spans chunks:
-                                // no partial batch at every chunk end (C2 m=16 -11%)
-#endif
 
 namespace hc {
 
 // ------------------------------------------------------------------ stream kernel
 // Small shifts (S <= 32), every text sector is read (f(m) = 1).  Each warp
-// owns a contiguous run of segments per chunk and stages exactly the chunk's lattice
-// q-gram bytes [k0 S + S - 1, k1 S + q - 2] into its own shared-memory buffer with
-// 16-byte cp.async copies (coalesced, L2-only), kStreamBufs - 1 chunks ahead of the
+// owns a contiguous run of segments per chunk and stages the chunk's lattice q-gram bytes
+// (plus those of the first steps) into its own shared-memory buffer, one chunk ahead of the
 // one it filters: no CTA-wide barrier, no hand-off between warps.  Phase A reads the
 // buffer; the lattice survivors go through first_steps and phase B on global text
 // (the chunk was just streamed through L2), exactly as on the gather path.
@@ -54,23 +48,21 @@ struct StreamQueue {
     uint32_t *q1;     // kStreamQ1 window ends a_k
     uint32_t *ctr;    // shared slot counter (= n1 between trips)
     uint32_t n1;      // warp-uniform count
-    // first steps of 32 queued survivors, on the chunk's stage (the queue only ever
-    // holds survivors of the chunk being filtered: it is drained at the chunk's end)
-    template <class TT>
+    // first steps of 32 queued survivors, on global text (the chunk was just streamed
+    // through L2; the queue spans chunks, so every batch but the last is full)
     __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
-                                            const TT &txt, uint32_t lane) {
+                                            uint32_t lane) {
         __syncwarp();
         const uint32_t e = q1[n1 - 32 + lane];
         n1 -= 32;
         __syncwarp();
         if (lane == 0) *ctr = n1;
         __syncwarp();
-        sink.steps_e_on(txt, true, e);
+        sink.steps_e(true, e);
     }
-    template <class TT>
     __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
-                                              const TT &txt, uint32_t lane) {
-        while (n1 >= 32) drain32(sink, txt, lane);
+                                              uint32_t lane) {
+        while (n1 >= 32) drain32(sink, lane);
         if (n1) {
             __syncwarp();
             const bool act = lane < n1;
@@ -79,7 +71,7 @@ struct StreamQueue {
             __syncwarp();
             if (lane == 0) *ctr = 0;
             __syncwarp();
-            sink.steps_e_on(txt, act, e);
+            sink.steps_e(act, e);
         }
     }
 };
@@ -126,11 +118,7 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             pos += kStreamUnroll * step;
         }
         if (qu.n1 < 32) break;
-#if HC_STREAM_GLOBAL_FS
-        qu.drain32(sink, sink.txt, lane);
-#else
-        qu.drain32(sink, txt, lane);
-#endif
+        qu.drain32(sink, lane);
     }
     for (; k < k1; k += 32, pos += step) {          // ragged tail, one round at a time
         const bool in = k + lane < k1;
@@ -141,53 +129,12 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             qu.n1 += __popc(bm);
             __syncwarp();
             if (lane == 0) *qu.ctr = qu.n1;
-#if HC_STREAM_GLOBAL_FS
-            if (qu.n1 >= 32) qu.drain32(sink, sink.txt, lane);
-#else
-            if (qu.n1 >= 32) qu.drain32(sink, txt, lane);
-#endif
+            if (qu.n1 >= 32) qu.drain32(sink, lane);
         }
     }
 }
 
-// cp.async variant (opts.tma_chunk < 0): 16-byte cp.async per lane; the first NB - 1
-// chunks were issued by the kernel's prologue (before the table load).
-template <int NB>
-__device__ __forceinline__ void stream_prologue(const KParams &p, uint32_t bufs0, uint32_t gw,
-                                                uint32_t total_warps, uint32_t lane) {
-#pragma unroll
-    for (int b = 0; b < NB - 1; ++b)
-        stream_issue(p, gw + b * total_warps, bufs0 + b * p.stage_bytes, lane);
-}
-template <int Q, int SH, int NB>
-__device__ __forceinline__ void stream_loop(const KParams &p, const PassBits &sF,
-                                            WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
-                                            StreamQueue<Q, SH> &qu, uint32_t bufs0,
-                                            uint32_t gw, uint32_t total_warps, uint32_t lane) {
-    const uint32_t y32 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.y));
-    uint32_t b = 0;
-    for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
-        // refill the buffer filtered last round with the chunk NB-1 ahead
-        const uint32_t bn = b == 0 ? NB - 1 : b - 1;
-        stream_issue(p, c + (NB - 1) * total_warps, bufs0 + bn * p.stage_bytes, lane);
-        cp_async_wait<NB - 1>();   // chunk c's group is complete (this lane's copies)
-        __syncwarp();              // ... and every lane's, visible to the warp
-        const StreamChunk g = stream_chunk(p, c);
-        const uint32_t buf = fence_value(bufs0 + b * p.stage_bytes);
-        const SmemText txt{buf + ((y32 + g.first) & 15u) - g.first};
-        if (!(kInstrument && p.debug == 1)) {   // debug 1: copy pipeline alone
-            stream_filter<Q, SH>(p, txt, sF, g.k0, g.k1, lane, qu, sink);
-#if !HC_STREAM_GLOBAL_FS
-            qu.drain_all(sink, txt, lane);
-#endif
-        }
-        __syncwarp();              // every lane is done with buffer b before its refill
-        b = b + 1 == NB ? 0 : b + 1;
-    }
-    cp_async_wait<0>();
-}
-
-// TMA variant (the default): each chunk moved by ONE 1-D bulk copy (cp.async.bulk, issued
+// Each chunk is moved by ONE 1-D bulk copy (cp.async.bulk, issued
 // by lane 0, completion on the buffer's mbarrier).  Interior chunks (all but the first and
 // the last few of the text) have a fixed geometry: chunk c holds lattice points
 // [c spc, (c+1) spc) and text bytes [first, first + D + max(q, 2q - S)), first = c D + m - 2q,
@@ -278,9 +225,6 @@ __device__ __forceinline__ void stream_loop_tma(const KParams &p, const PassBits
             }
             const SmemText txt{buf + ((ts.y32 + f) & 15u) - f};
             stream_filter<Q, SH>(p, txt, sF, k0, k1, lane, qu, sink);
-#if !HC_STREAM_GLOBAL_FS
-            qu.drain_all(sink, txt, lane);
-#endif
         }
         __syncwarp();              // every lane is done with buffer b before its refill
         b = b + 1 == NB ? 0 : b + 1;
@@ -361,13 +305,7 @@ __global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KPar
     const TmaStream ts{yaddr, static_cast<uint32_t>(yaddr), p.seg_per_chunk * p.S,
                        p.seg_per_chunk * p.S + max(p.q, 2 * p.q - min(p.S, 2 * p.q)), bufs0, p.stage_bytes,
                        reinterpret_cast<uint64_t *>(smem + L.ctr_off + round_up(NW * 4u, 8)) + warp * 4};
-    if (p.tma_chunk) {
-        if (p.stages == 4) stream_prologue_tma<4>(p, ts, gw, total_warps, lane);
-        else if (p.stages == 3) stream_prologue_tma<3>(p, ts, gw, total_warps, lane);
-        else stream_prologue_tma<2>(p, ts, gw, total_warps, lane);
-    } else if (p.stages == 2) stream_prologue<2>(p, bufs0, gw, total_warps, lane);
-    else if (p.stages == 3) stream_prologue<3>(p, bufs0, gw, total_warps, lane);
-    else stream_prologue<4>(p, bufs0, gw, total_warps, lane);
+    stream_prologue_tma<2>(p, ts, gw, total_warps, lane);
     load_pass_bits(p, reinterpret_cast<uint32_t *>(smem + L.bits_off));
     load_table(p, sFp, sx);
     if (tid == 0) s_params[0] = p;
@@ -385,29 +323,20 @@ __global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KPar
     if (lane == 0) *ctr = 0;
     __syncwarp();
     StreamQueue<Q, SH> qu{reinterpret_cast<uint32_t *>(smem + L.q_off) + warp * kStreamQ1, ctr, 0u};
-    if (p.tma_chunk) {
-        if (p.stages == 4)
-            stream_loop_tma<Q, SH, 4>(p, pb, sink, qu, ts, gw, total_warps, lane);
-        else if (p.stages == 3)
-            stream_loop_tma<Q, SH, 3>(p, pb, sink, qu, ts, gw, total_warps, lane);
-        else
-            stream_loop_tma<Q, SH, 2>(p, pb, sink, qu, ts, gw, total_warps, lane);
-    } else if (p.stages == 2)
-        stream_loop<Q, SH, 2>(p, pb, sink, qu, bufs0, gw, total_warps, lane);
-    else if (p.stages == 3)
-        stream_loop<Q, SH, 3>(p, pb, sink, qu, bufs0, gw, total_warps, lane);
-    else
-        stream_loop<Q, SH, 4>(p, pb, sink, qu, bufs0, gw, total_warps, lane);
+    // two buffers per warp (3 and 4 measured slower at every m: DESIGN.md 5; fewer loop
+    // variants also keep the kernel's code small)
+    stream_loop_tma<Q, SH, 2>(p, pb, sink, qu, ts, gw, total_warps, lane);
     path_ts(p, 3);
+#ifndef HC_NO_BOXES
     if (p.slot_bytes) {
         __syncwarp();
         final_drain_boxes<Q, SH>(p, sF, sx, qu.q1, qu.n1, sink.q2, sink.n2, bufs0, wo, lane);
         qu.n1 = 0;
         sink.n2 = 0;
-    } else {
-#if HC_STREAM_GLOBAL_FS
-        qu.drain_all(sink, gtxt, lane);
+    } else
 #endif
+    {
+        qu.drain_all(sink, lane);
         path_ts(p, 4);
         sink.drain();
     }

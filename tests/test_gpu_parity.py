@@ -492,11 +492,11 @@ def test_long_patterns(path):
     assert ei.value.code == hc.HC_ETOOLONG
 
 
-def test_stream_copy_variants():
-    """The stream path's two chunk copies: one 1-D TMA bulk copy per chunk (the default) and
-    16-byte cp.async per lane (opts.tma_chunk < 0): unaligned texts, edge chunks (the first
-    chunk, the last chunks, texts ending inside a 16-byte word), shifts below q (m < 2q),
-    2 and 3 buffers, small chunks (many interior chunks per warp), against brute force."""
+def test_stream_chunk_copies():
+    """The stream path's chunk copies (one 1-D TMA bulk copy per chunk): unaligned texts,
+    edge chunks (the first chunk, the last chunks, texts ending inside a 16-byte word),
+    shifts below q (m < 2q), small chunks (many interior chunks per warp), few warps per
+    CTA, both final drains, against brute force."""
     rng = np.random.default_rng(79)
     for n in (1000, 70_001, 1_000_003):
         y = I.gen_text("dna", n, 79 + n % 7)
@@ -505,13 +505,12 @@ def test_stream_copy_variants():
             x = y[o:o + m].copy()
             want = oracle.brute(x, y)
             for off in (0, 5, 15):
-                for stages in (2, 3):
-                    for tma, tile, spl in ((0, 0, 0), (-1, 0, 0), (0, 700, 0), (-1, 700, -1), (0, 0, -1)):
-                        # seg_per_lane < 0: final drain on global text instead of private boxes
-                        got = gpu(hc.prepare(x, q, 12), to_dev(y, off), path=hc.PATH_STREAM,
-                                  tma_chunk=tma, stages=stages, tile_bytes=tile,
-                                  max_ctas=3 if tile else 0, seg_per_lane=spl)
-                        assert np.array_equal(got, want), (n, m, off, stages, tma, tile, spl)
+                for bw, tile, spl in ((0, 0, 0), (8, 0, 0), (0, 700, 0), (3, 700, -1), (0, 0, -1)):
+                    # seg_per_lane < 0: final drain on global text instead of private boxes
+                    got = gpu(hc.prepare(x, q, 12), to_dev(y, off), path=hc.PATH_STREAM,
+                              block_warps=bw, tile_bytes=tile, max_ctas=3 if tile else 0,
+                              seg_per_lane=spl)
+                    assert np.array_equal(got, want), (n, m, off, bw, tile, spl)
 
 
 def test_epilogue_ordering_any_block_size():
