@@ -37,38 +37,40 @@ int gather_smem_bytes(uint32_t alpha, uint32_t m) {
 // chunk's loads are issued before this chunk's survivors are handed to the sink
 // (first steps / phase B round trips), so they overlap.  The first chunk's loads are
 // issued before the table load (`W` comes in loaded).
-template <int Q, int SH, int L, class Sink>
+template <int Q, int SH, class Sink>
 __device__ __forceinline__ void gather_loop(const KParams &p, const GlobalText &txt, const FBits &fb,
                                             uint32_t c, uint32_t total_warps, uint32_t lane,
-                                            uint64_t (&W)[4], Sink &sink, uint64_t *bar,
+                                            uint32_t L, uint64_t (&W)[4], Sink &sink, uint64_t *bar,
                                             bool &ready) {
+    // ONE copy of the loop for L = 1, 2, 4 (rounds u >= L are skipped by warp-uniform tests):
+    // three specialised copies tripled the kernel's code, and code size is time here (the
+    // kernel runs for 30-60 us and fetches most of its instructions exactly once).
     const uint32_t step = 32 * p.S;
     while (c < p.nchunks) {
         const uint32_t k0 = c * 32 * L;
         const uint32_t pos0 = p.m - 1 + (k0 + lane) * p.S;
-        bool pass[L];
-        bool any = false;
+        uint32_t pm = 0;                           // bit u: round u's lattice point passes
 #pragma unroll
-        for (int u = 0; u < L; ++u) {
-            pass[u] = k0 + u * 32 + lane < p.K && fb.pass(qhash<Q, SH>(W[u], p.mask));   // l.4-6
-            any |= pass[u];
-        }
+        for (uint32_t u = 0; u < 4; ++u)
+            pm |= static_cast<uint32_t>(u < L && k0 + u * 32 + lane < p.K &&
+                                        fb.pass(qhash<Q, SH>(W[u], p.mask))) << u;   // l.4-6
         c += total_warps;
         if (c < p.nchunks) {                       // next chunk's loads, before the survivors
             const uint32_t kn = c * 32 * L + lane;
 #pragma unroll
-            for (int u = 0; u < L; ++u)
-                W[u] = kn + u * 32 < p.K ? end8<Q>(txt, p.m - 1 + (kn + u * 32) * p.S) : 0ull;
+            for (uint32_t u = 0; u < 4; ++u)
+                if (u < L) W[u] = kn + u * 32 < p.K ? end8<Q>(txt, p.m - 1 + (kn + u * 32) * p.S) : 0ull;
         }
-        if (__any_sync(HC_FULL, any)) {
+        if (__any_sync(HC_FULL, pm != 0)) {
             if (!ready) {                          // F and x (TMA bulk copy) are needed now
                 mbar_wait(bar, 0);
                 ready = true;
             }
-#pragma unroll
-            for (int u = 0; u < L; ++u) {
-                const uint32_t bm = __ballot_sync(HC_FULL, pass[u]);
-                if (bm) sink(bm, pass[u], pos0 + u * step);
+#pragma unroll 1
+            for (uint32_t u = 0; u < L; ++u) {     // one copy of the sink's code
+                const bool pass = (pm >> u) & 1u;
+                const uint32_t bm = __ballot_sync(HC_FULL, pass);
+                if (bm) sink(bm, pass, pos0 + u * step);
             }
         }
     }
@@ -127,12 +129,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p)
     bool ready = false;
     path_ts(p, 1);
     if (kInstrument && lane == 0) trace_event(p, warp, 0);          // bitmap loaded
-    if (L >= 4)
-        gather_loop<Q, SH, 4>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
-    else if (L == 2)
-        gather_loop<Q, SH, 2>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
-    else
-        gather_loop<Q, SH, 1>(p, txt, fb, c0, total_warps, lane, W, sink, bar, ready);
+    gather_loop<Q, SH>(p, txt, fb, c0, total_warps, lane, L, W, sink, bar, ready);
     path_ts(p, 3);
     if (!ready) mbar_wait(bar, 0);
     path_ts(p, 4);
