@@ -48,31 +48,25 @@ struct StreamQueue {
     uint32_t *q1;     // kStreamQ1 window ends a_k
     uint32_t *ctr;    // shared slot counter (= n1 between trips)
     uint32_t n1;      // warp-uniform count
-    // first steps of 32 queued survivors, on global text (the chunk was just streamed
-    // through L2; the queue spans chunks, so every batch but the last is full)
+    // first steps of up to 32 queued survivors (the last ones queued), on global text (the
+    // chunk was just streamed through L2; the queue spans chunks, so every batch but the
+    // last is full)
     __device__ __forceinline__ void drain32(WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
                                             uint32_t lane) {
         __syncwarp();
-        const uint32_t e = q1[n1 - 32 + lane];
-        n1 -= 32;
+        const uint32_t cnt = min(n1, 32u);
+        const bool act = lane < cnt;
+        const uint32_t e = act ? q1[n1 - cnt + lane] : 0u;
+        n1 -= cnt;
         __syncwarp();
         if (lane == 0) *ctr = n1;
         __syncwarp();
-        sink.steps_e(true, e);
+        sink.steps_e(act, e);
     }
     __device__ __forceinline__ void drain_all(WarpQueueSink<Q, SH, GlobalText, FTable> &sink,
                                               uint32_t lane) {
-        while (n1 >= 32) drain32(sink, lane);
-        if (n1) {
-            __syncwarp();
-            const bool act = lane < n1;
-            const uint32_t e = act ? q1[lane] : 0u;
-            n1 = 0;
-            __syncwarp();
-            if (lane == 0) *ctr = 0;
-            __syncwarp();
-            sink.steps_e(act, e);
-        }
+#pragma unroll 1
+        while (n1) drain32(sink, lane);
     }
 };
 
@@ -120,7 +114,9 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
         if (qu.n1 < 32) break;
         qu.drain32(sink, lane);
     }
-    for (; k < k1; k += 32, pos += step) {          // ragged tail, one round at a time
+    // ragged tail, one round at a time; no drain here (the queue holds 32 * (unroll + 1):
+    // < 32 on entry plus fewer than `unroll` rounds), the next chunk's loop drains first
+    for (; k < k1; k += 32, pos += step) {
         const bool in = k + lane < k1;
         const bool pass = in && sF.pass(qhash<Q, SH>(end8<Q>(txt, pos), p.mask));
         const uint32_t bm = __ballot_sync(HC_FULL, pass);
@@ -129,7 +125,6 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             qu.n1 += __popc(bm);
             __syncwarp();
             if (lane == 0) *qu.ctr = qu.n1;
-            if (qu.n1 >= 32) qu.drain32(sink, lane);
         }
     }
 }
