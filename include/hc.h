@@ -111,8 +111,7 @@ typedef struct hc_search_opts {
     int path;         /* hc_path */
     int tile_bytes;   /* staged: text bytes per shared-memory stage; stream: target text bytes
                          per warp chunk (0 = default) */
-    int stages;       /* staged: TMA pipeline depth; multi-pattern stream launches: buffers per
-                         warp, 2 or 3 (the single-pattern stream kernel always uses 2) */
+    int stages;       /* staged: TMA pipeline depth (the stream kernels always use 2 buffers per warp) */
     int seg_per_lane; /* gather: segments handed to each lane per chunk (0 = default);
                          stream: < 0 = final drain on global text (no private boxes) */
     int max_ctas;     /* cap on the persistent grid (0 = no cap; tests use 1..3 for many tiles per CTA) */

@@ -909,7 +909,7 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
                 if (stream_multi) {
                     p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))
                                                       : (g > 2 ? 16u : 8u);
-                    p.stages = o.stages == 3 ? 3u : 2u;   // multi-pattern kernel: 2 or 3 buffers
+                    p.stages = 2;   // multi-pattern kernel: 2 buffers per warp
                 } else {   // gather access, no stage buffers
                     p.mgather = 1;
                     p.block_warps = o.block_warps > 0 ? std::min<uint32_t>(16u, static_cast<uint32_t>(o.block_warps))

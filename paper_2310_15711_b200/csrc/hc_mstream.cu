@@ -232,9 +232,7 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
             mstream_filter<Q, SH, GlobalText>(p, gtxt, P, k0, min(k0 + p.seg_per_chunk, p.K), lane, mw,
                                               sx0, L.x_stride);
         }
-    } else if (p.stages == 3)
-        mstream_loop<Q, SH, 3>(p, P, mw, sx0, L.x_stride, bufs0, gw, total_warps, lane);
-    else
+    } else   // two buffers per warp (one loop variant: code size is time)
         mstream_loop<Q, SH, 2>(p, P, mw, sx0, L.x_stride, bufs0, gw, total_warps, lane);
     // queued survivors, phase B leftovers and output buffers of every pattern
     __syncwarp();
