@@ -82,7 +82,10 @@ __device__ __forceinline__ void gather_loop(const KParams &p, const GlobalText &
 // when it first has survivors.  Every warp waits before the end, so the copy has landed
 // before the epilogue reuses the shared memory.
 template <int Q, int SH>
-__global__ void __launch_bounds__(kGatherThreads) gather_kernel(const KParams p) {
+// Registers: q-grams of up to 4 bytes hash from one 32-bit half and fit 64 registers, i.e. 4
+// CTAs per SM (A/B: C3/C4 m = 128..1024, q = 3 or 4: 7-8% faster than at 80 registers and 3
+// CTAs); longer q-grams spill there (C2, q = 6 or 8: 5-11% slower) and get up to 85 (3 CTAs).
+__global__ void __launch_bounds__(kGatherThreads, Q <= 4 ? 4 : 3) gather_kernel(const KParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t NW = kGatherThreads / 32;
     const GatherLayout Lo = gather_layout(p.alpha, p.m, NW);
