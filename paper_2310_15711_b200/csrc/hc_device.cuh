@@ -177,6 +177,15 @@ struct GlobalText {
         return __ldg(reinterpret_cast<const unsigned long long *>(aligned));
 #endif
     }
+    __device__ __forceinline__ uint32_t word32(uintptr_t aligned) const {
+#if HC_LDG_MODE >= 1
+        uint32_t r;
+        asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(r) : "l"(aligned));
+        return r;
+#else
+        return __ldg(reinterpret_cast<const unsigned int *>(aligned));
+#endif
+    }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return __ldg(y + p); }
     __device__ __forceinline__ GlobalText shfl(uint32_t) const { return *this; }  // same in all lanes
     static constexpr bool kLoSafe = false;  // the word before may be outside y
@@ -212,6 +221,7 @@ struct SmemText {
     uint32_t base;
     __device__ __forceinline__ uint32_t addr(uint32_t p) const { return base + p; }
     __device__ __forceinline__ uint64_t word(uint32_t aligned) const { return lds64(aligned); }
+    __device__ __forceinline__ uint32_t word32(uint32_t aligned) const { return lds32(aligned); }
     __device__ __forceinline__ uint32_t byte(uint32_t p) const { return lds8(base + p); }
     // lane L's mapping (survivor boxes: every lane has its own)
     __device__ __forceinline__ SmemText shfl(uint32_t L) const {
@@ -276,6 +286,18 @@ template <int Q, class T>
 __device__ __forceinline__ uint64_t end8(const T &t, uint32_t p) {
     auto a = t.addr(p);
     using A = decltype(a);
+    if constexpr (Q <= 4) {
+        // q-grams of up to 4 bytes: the two aligned 4-byte words and one funnel shift (the
+        // hash reads only the upper half of the result)
+        const A a4 = a & ~static_cast<A>(3);
+        const uint32_t off = static_cast<uint32_t>(a & 3);
+        const uint32_t hi = t.word32(a4);
+        uint32_t lo = 0;
+        if constexpr (Q > 1) {
+            if (T::kLoSafe || off + 1 < static_cast<uint32_t>(Q)) lo = t.word32(a4 - 4);
+        }
+        return static_cast<uint64_t>(__funnelshift_l(lo, hi, 24 - 8 * off)) << 32;
+    }
     const A ah = a & ~static_cast<A>(7);
     const uint32_t off = static_cast<uint32_t>(a & 7);
     const uint64_t hi = t.word(ah);
