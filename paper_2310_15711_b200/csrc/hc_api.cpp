@@ -773,7 +773,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
         }
 #endif
         if (HC_INSTRUMENT && (o.debug == 5 || o.debug == 10) && stats) {
-            cudaMemcpy(stats->dbg, sc->buf + (o.debug == 5 ? 4 : 6), 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(stats->dbg, sc->buf + 6, 8, cudaMemcpyDeviceToHost);
             cudaMemset(sc->buf + 4, 0, 16);
         }
         if (want_pos && count > cap) {

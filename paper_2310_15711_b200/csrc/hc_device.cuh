@@ -468,6 +468,7 @@ struct WarpOut {
             base = __shfl_sync(HC_FULL, base, 0);
             const uint32_t v = buf[lane];
             if (base + lane < p.cap) p.out[base + lane] = v;
+            if (base + lane == 0) p.counter[4] = v;   // the first slot's position (epilogue)
             const uint32_t rest = cnt - 32;
             const uint32_t nv = lane < rest ? buf[32 + lane] : 0u;
             __syncwarp();
@@ -483,6 +484,7 @@ struct WarpOut {
         if (lane == 0) base = atomicAdd(p.counter, cnt);
         base = __shfl_sync(HC_FULL, base, 0);
         if (lane < cnt && base + lane < p.cap) p.out[base + lane] = buf[lane];
+        if (base + lane == 0) p.counter[4] = buf[0];  // the first slot's position (epilogue)
         __syncwarp();
         cnt = 0;
     }
@@ -511,7 +513,7 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
     uint32_t e = 0, i = 0, z = 0, v = 0, wsteps = 0;
     bool walk = false;
     const bool long_walks = p.m >= 2 * kLongWalk * Q;   // warp-wide walks can pay off
-    if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 5, 1u);
+    if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 7, 1u);
     // Walk-heavy text (allow_abort, gather path): Fig. 5's loop would re-hash most q-grams
     // many times over (the stress config C5: ~7 hashes per text byte).  A batch that needs
     // more than kAbortWalks warp-wide walks raises the give-up flag, and every later
@@ -521,7 +523,7 @@ __device__ __noinline__ uint32_t run_segments_impl(const T txt, const FT sF, con
     // on non-repetitive text) read the flag.
     uint32_t nwalks = 0, nit = 0;
     while (__any_sync(HC_FULL, active)) {
-        if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 4, 1u);
+        if (kInstrument && p.debug == 5 && lane == 0) atomicAdd(p.counter + 6, 1u);
         path_cnt(p, 0, lane);
         path_ts(p, 9 + min(nit++, 6u));
         bool need_v = false, stepped = false;
@@ -1125,15 +1127,16 @@ __device__ __forceinline__ bool cta_is_last(uint32_t *ticket) {
 
 // The last CTA's work for one search: publish, order when possible, reset the counters.
 // `smem` is the CTA's dynamic shared memory (idle by now), `smem_bytes` its size.
+// `count` and `pos0` (the position in slot 0 of the scratch, counter[4]) were read by the
+// caller together with the give-up flag: one round trip after the ticket, not three.
 __device__ __forceinline__ void publish_search(uint32_t *counter, const uint32_t *out, uint32_t cap,
                                                uint32_t *host_count, int64_t *dst, uint32_t k_out,
                                                uint32_t epi_cap, uint8_t *smem, bool fault,
-                                               uint32_t nbits) {
-    const uint32_t count = *reinterpret_cast<volatile uint32_t *>(counter);
+                                               uint32_t nbits, uint32_t count, uint32_t pos0) {
     bool ordered = count == 0 || dst == nullptr || k_out == 0;
     if (!ordered && count <= cap && count <= epi_cap) {
         if (count == 1) {
-            if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(__ldcg(out));
+            if (threadIdx.x == 0) dst[0] = static_cast<int64_t>(pos0);
             ordered = true;
         } else {
             unsigned long long t0 = 0;
@@ -1171,7 +1174,12 @@ __device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem)
     const bool last_cta = cta_is_last(p.counter + 2);
     path_ts(p, 7);
     if (!last_cta) return;
-    if (*reinterpret_cast<volatile uint32_t *>(p.counter + 3)) {
+    // count, give-up flag and the first position in ONE round trip (independent loads)
+    uint32_t c0, c3, pos0;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(c0) : "l"(p.counter));
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(c3) : "l"(p.counter + 3));
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(pos0) : "l"(p.counter + 4));
+    if (c3) {
         // the search gave up (walk-heavy text, see gather_kernel): the host re-runs it on
         // the scan path; nothing of this run is published but the verdict
         if (threadIdx.x == 0) {
@@ -1182,7 +1190,7 @@ __device__ __forceinline__ void search_epilogue(const KParams &p, uint8_t *smem)
         return;
     }
     publish_search(p.counter, p.out, p.cap, p.host_count, p.dst, p.k_out, p.epi_cap, smem,
-                   p.debug == 9, p.nbits);
+                   p.debug == 9, p.nbits, c0, pos0);
     __syncthreads();
     if (threadIdx.x == 0) p.counter[2] = 0;
     path_ts(p, 8);

@@ -38,7 +38,8 @@ struct KParams {
     uint32_t cap;        // capacity of out
     uint32_t *counter;   // kCtr words: [0] = total occurrences (may exceed cap), [1] = staged
                          // tile counter, [2] = CTAs done (epilogue ticket), [3] = give-up
-                         // flag (gather); zero between calls
+                         // flag (gather); zero between calls.  [4] = the position in slot 0
+                         // of out (read by the epilogue with the count)
     // fused epilogue (the last CTA to finish): count publication + ordering
     uint32_t *host_count;  // mapped pinned [2]: count, then 1 if the positions were ordered
                            // into dst by the epilogue (else the host orders them)

@@ -253,8 +253,10 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
     // fused epilogue: the last CTA publishes and orders every pattern's positions
     if (cta_is_last(mp.counter[0] + 2)) {
         for (uint32_t i = 0; i < P; ++i) {
+            const uint32_t cnt_i = *reinterpret_cast<volatile uint32_t *>(mp.counter[i]);
+            const uint32_t pos0_i = *reinterpret_cast<volatile uint32_t *>(mp.counter[i] + 4);
             publish_search(mp.counter[i], mp.out[i], mp.cap[i], mp.host_count[i], mp.dst[i],
-                           mp.k_out[i], p.epi_cap, smem, p.debug == 9, p.nbits);
+                           mp.k_out[i], p.epi_cap, smem, p.debug == 9, p.nbits, cnt_i, pos0_i);
             __syncthreads();
         }
         if (tid == 0) mp.counter[0][2] = 0;

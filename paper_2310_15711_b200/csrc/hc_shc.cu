@@ -30,6 +30,7 @@ int shc_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t box_
 __device__ __forceinline__ void shc_output(const KParams &p, uint32_t pos) {
     const uint32_t slot = atomicAdd(p.counter, 1u);
     if (slot < p.cap) p.out[slot] = pos;
+    if (slot == 0) p.counter[4] = pos;   // the first slot's position (epilogue)
 }
 
 template <int Q, int SH>

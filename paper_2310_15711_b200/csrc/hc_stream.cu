@@ -276,6 +276,74 @@ __device__ __forceinline__ void final_drain_boxes(const KParams &p, const FTable
     }
 }
 
+// The stream kernel's tables: the filter bitmap (replicated per lane or not), F and x.  Every
+// thread issues ALL its global loads (one bitmap word, two 16-byte vectors of F, one of x)
+// before its first shared store: one DRAM round trip for the lot (after the L2 flush of the
+// bench every one of them is a miss), where load_pass_bits + load_table took three in a row.
+// What a 768-thread block cannot cover that way (alpha > 13 at fewer warps, m > 12 K) follows
+// in plain loops.
+__device__ __forceinline__ void stream_load_tables(const KParams &p, uint32_t *bits, uint32_t *sF,
+                                                   uint8_t *sx) {
+    const uint32_t T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, NW = T >> 5;
+    const uint32_t nF = 1u << p.alpha;
+    const uint32_t nw = nF > 32 ? nF / 32 : 1u;          // bitmap words
+    if (nF < 8) {                                        // tiny tables: the plain loaders
+        load_pass_bits(p, bits);
+        load_table(p, sF, sx);
+        return;
+    }
+    const uint32_t n4 = nF / 4;                          // 16-byte vectors of F
+    const uint32_t n16 = (p.m + 8 + 15) / 16;            // ... and of x (zero-padded past m)
+    const uint4 *F4 = reinterpret_cast<const uint4 *>(p.F);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(p.x);
+    // loads
+    uint32_t bw = 0;
+    if (p.lane_bits) {
+        if (warp * 32 + lane < nw) bw = __ldg(p.Fbits + warp * 32 + lane);
+    } else if (t < nw) {
+        bw = __ldg(p.Fbits + t);
+    }
+    uint4 fv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+#pragma unroll
+    for (uint32_t r = 0; r < 2; ++r)
+        if (t + r * T < n4) fv[r] = __ldg(F4 + t + r * T);
+    uint4 xv = make_uint4(0, 0, 0, 0);
+    if (t < n16 && 16 * t < p.m) xv = __ldg(x4 + t);
+    // stores
+    if (p.lane_bits) {
+        if (warp * 32 < nw) {
+            const uint32_t cnt = min(32u, nw - warp * 32);
+            for (uint32_t k = 0; k < cnt; ++k) bits[(warp * 32 + k) * 32 + lane] = __shfl_sync(HC_FULL, bw, k);
+        }
+        for (uint32_t base = (warp + NW) * 32; base < nw; base += NW * 32) {   // alpha > 10 + log2(NW)
+            const uint32_t v = base + lane < nw ? __ldg(p.Fbits + base + lane) : 0u;
+            const uint32_t cnt = min(32u, nw - base);
+            for (uint32_t k = 0; k < cnt; ++k) bits[(base + k) * 32 + lane] = __shfl_sync(HC_FULL, v, k);
+        }
+    } else {
+        if (t < nw) bits[t] = bw;
+        for (uint32_t i = t + T; i < nw; i += T) bits[i] = __ldg(p.Fbits + i);
+    }
+    uint4 *dF = reinterpret_cast<uint4 *>(sF);
+#pragma unroll
+    for (uint32_t r = 0; r < 2; ++r)
+        if (t + r * T < n4) dF[t + r * T] = fv[r];
+    for (uint32_t w = t + 2 * T; w < n4; w += T) dF[w] = __ldg(F4 + w);
+    for (uint32_t w = t; w < n16; w += T) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (w == t) v = xv;
+        else if (16 * w < p.m) v = __ldg(x4 + w);
+        uint32_t *vw = reinterpret_cast<uint32_t *>(&v);
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {               // zero from byte m on (8-byte compares of x)
+            const uint32_t b = 16 * w + 4 * j;
+            if (b >= p.m) vw[j] = 0;
+            else if (b + 4 > p.m) vw[j] &= (1u << (8 * (p.m - b))) - 1u;
+        }
+        reinterpret_cast<uint4 *>(sx)[w] = v;
+    }
+}
+
 template <int Q, int SH>
 #ifndef HC_STREAM_MINB
 #define HC_STREAM_MINB 3
@@ -301,8 +369,7 @@ __global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KPar
                        p.seg_per_chunk * p.S + max(p.q, 2 * p.q - min(p.S, 2 * p.q)), bufs0, p.stage_bytes,
                        reinterpret_cast<uint64_t *>(smem + L.ctr_off + round_up(NW * 4u, 8)) + warp * 4};
     stream_prologue_tma<2>(p, ts, gw, total_warps, lane);
-    load_pass_bits(p, reinterpret_cast<uint32_t *>(smem + L.bits_off));
-    load_table(p, sFp, sx);
+    stream_load_tables(p, reinterpret_cast<uint32_t *>(smem + L.bits_off), sFp, sx);
     if (tid == 0) s_params[0] = p;
     __syncthreads();
     path_ts(p, 1);
