@@ -130,7 +130,9 @@ typedef struct hc_search_opts {
     int trace_tiles;
     int surv_warps;   /* staged: survivor/producer warps per CTA (0 = default) */
     int block_warps;  /* stream: warps per CTA, 1..24 (0 = default: up to 24, one CTA per SM) */
-    int no_multi;     /* hc_search_batch: 1 = no multi-pattern launches (each pattern alone) */
+    int no_multi;     /* hc_search_batch: 0 = multi-pattern launches for shifts 9..256 (measured
+                         faster there), 1 = never (each pattern alone), 2 = whenever the
+                         patterns' shapes allow (shifts <= 256) */
 } hc_search_opts;
 
 typedef struct hc_search_stats {
@@ -155,7 +157,7 @@ int64_t hc_search_ex(const hc_handle *h, const uint8_t *y_dev, size_t n, int64_t
 /* Batch of independent searches over the same text (multi-pattern
  * batching): the result of pattern i is exactly hc_search(hs[i], y_dev, n, pos_out[i],
  * max_out[i], stream) (Fig. 5, per pattern).  Consecutive patterns of
- * equal (m, q, alpha) with shifts m - q + 1 <= 256 are searched up to 4 per launch by
+ * equal (m, q, alpha) with shifts 9 <= m - q + 1 <= 256 are searched up to 4 per launch by
  * the multi-pattern kernel: one pass over the text, each lattice q-gram hashed once
  * and tested against every pattern's F (opts->no_multi = 1 disables it).  Launches
  * are spread over 8 library-owned streams so that one launch's tail and launch

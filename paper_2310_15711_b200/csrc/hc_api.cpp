@@ -245,6 +245,9 @@ constexpr uint32_t kShcLaneBytes = 128;         // SHC path: text bytes per lane
 // hc_search_batch: patterns of equal (m, q, alpha) with shifts up to this share one
 // streamed pass over the text (multi-pattern stream kernel)
 constexpr uint32_t kMultiMaxShift = 32;
+// ... and from this shift up: below it the survivors dominate and separate searches on the
+// library's streams are faster (C2 m = 8: 87 vs 116 us per pattern; C3/C4 m <= 8 as well)
+constexpr uint32_t kMultiMinShift = 9;
 // ... and with the gather access (the patterns share the lattice's DRAM sectors) up to
 #ifndef HC_MULTI_GATHER_MAX_SHIFT
 #define HC_MULTI_GATHER_MAX_SHIFT 256
@@ -886,7 +889,8 @@ int hc_search_batch(const hc_handle *const *hs, size_t npat, const uint8_t *y_de
         size_t g = 1;
         const bool stream_multi = S <= kMultiMaxShift;
         const int multi_path = stream_multi ? HC_PATH_STREAM : HC_PATH_GATHER;
-        const bool multi_ok = !o.no_multi && S <= kMultiGatherMaxShift &&
+        const bool multi_ok = (o.no_multi == 2 || (o.no_multi == 0 && S >= kMultiMinShift)) &&
+                              S <= kMultiGatherMaxShift &&
                               (o.path == HC_PATH_AUTO || o.path == multi_path);
         if (multi_ok)
             while (i + g < npat && g < static_cast<size_t>(hc::kMaxPatterns) && hs[i + g] &&

@@ -328,7 +328,7 @@ def test_ordering_paths(path):
         assert np.array_equal(got, want), (count, packed, len(got))
 
 
-@pytest.mark.parametrize("no_multi", [0, 1])
+@pytest.mark.parametrize("no_multi", [0, 1, 2])
 def test_search_batch_multi_pattern_groups(no_multi):
     """Multi-pattern launches (patterns sharing m, q, alpha filtered in one pass over the
     text; staged for shifts <= 32, gather access up to 256, single beyond): groups of
