@@ -1,3 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/tq.log 2>&1; echo rc=$? >> gpurun_out/tq.log
-python tools/batch_bench.py --config C2 --ms 8 16 2>&1 | tail -2
-python tools/batch_bench.py --config C4 --ms 4 8 2>&1 | tail -2
+for g in 0 32 128; do
+echo "== HC_L2_FETCH=$g"
+if [ $g = 0 ]; then unset HC_L2_FETCH; else export HC_L2_FETCH=$g; fi
+python tools/profile_search.py --config C2 --m 32 64 128 256 512 1024 --reps 6 2>&1 | grep "rep=[345]\|libhc" | awk '{print $1, $6}' | paste -sd' '
+done
