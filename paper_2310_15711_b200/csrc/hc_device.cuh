@@ -94,9 +94,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void chk_shared(uint32_t a, uint32_t bytes);   // instrumented build
 // 1-D TMA bulk copy global -> shared, completion signalled on `bar` (tx bytes).
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {
+#if HC_INSTRUMENT
+    chk_shared(dst, 16);
+    chk_shared(dst + bytes - 16, 16);
+    if ((bytes & 15) || (reinterpret_cast<uintptr_t>(src) & 15)) __trap();
+#endif
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             dst),
@@ -159,12 +165,48 @@ __device__ __forceinline__ uint64_t shl64(uint64_t a, uint32_t s) {
 
 // ------------------------------------------------------------------ text access
 // Text byte p (0 <= p < n) of y, read from global memory (read-only path).
+// Instrumented build: every text access is bounds-checked (compute-sanitizer is closed on
+// this GPU pool, so the memcheck is our own): an aligned global word must hold at least one
+// byte of [y, y + n), a shared access must lie inside the CTA's shared memory, copies into
+// shared memory must read inside the text.  A violation traps: the parity driver of
+// tests/test_gpu_tools.py (every path, small inputs, exact-size texts) then fails.
+__device__ __forceinline__ void chk_fail() {
+#if HC_INSTRUMENT
+    __trap();
+#endif
+}
+#if HC_INSTRUMENT
+extern __shared__ __align__(128) uint8_t hc_chk_dyn_smem[];   // the kernels' dynamic shared memory
+#endif
+__device__ __forceinline__ void chk_shared(uint32_t a, uint32_t bytes) {
+#if HC_INSTRUMENT
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const uint32_t lo = static_cast<uint32_t>(__cvta_generic_to_shared(hc_chk_dyn_smem));
+    if (a < lo || a + bytes > lo + dyn || (a & (bytes - 1))) chk_fail();
+#endif
+}
+__device__ __forceinline__ void chk_text_range(const uint8_t *y, uint32_t n, uintptr_t a, uint32_t bytes) {
+#if HC_INSTRUMENT
+    if (a < reinterpret_cast<uintptr_t>(y) || a + bytes > reinterpret_cast<uintptr_t>(y) + n) chk_fail();
+#endif
+}
 struct GlobalText {
     const uint8_t *y;
+#if HC_INSTRUMENT
+    uint32_t n = 0;   // text length: accesses are checked when set
+    __device__ __forceinline__ void chk(uintptr_t a, uint32_t bytes) const {
+        const uintptr_t y0 = reinterpret_cast<uintptr_t>(y);
+        if (n && (a + bytes <= y0 || a >= y0 + n || (a & (bytes - 1)))) chk_fail();
+    }
+#else
+    __device__ __forceinline__ void chk(uintptr_t, uint32_t) const {}
+#endif
     __device__ __forceinline__ uintptr_t addr(uint32_t p) const {
         return reinterpret_cast<uintptr_t>(y) + p;
     }
     __device__ __forceinline__ uint64_t word(uintptr_t aligned) const {
+        chk(aligned, 8);
 #if HC_LDG_MODE == 1
         uint64_t r;
         asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(r) : "l"(aligned));
@@ -178,6 +220,7 @@ struct GlobalText {
 #endif
     }
     __device__ __forceinline__ uint32_t word32(uintptr_t aligned) const {
+        chk(aligned, 4);
 #if HC_LDG_MODE >= 1
         uint32_t r;
         asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(r) : "l"(aligned));
@@ -186,25 +229,40 @@ struct GlobalText {
         return __ldg(reinterpret_cast<const unsigned int *>(aligned));
 #endif
     }
-    __device__ __forceinline__ uint32_t byte(uint32_t p) const { return __ldg(y + p); }
+    __device__ __forceinline__ uint32_t byte(uint32_t p) const {
+        chk(reinterpret_cast<uintptr_t>(y) + p, 1);
+        return __ldg(y + p);
+    }
     __device__ __forceinline__ GlobalText shfl(uint32_t) const { return *this; }  // same in all lanes
     static constexpr bool kLoSafe = false;  // the word before may be outside y
 };
+
+// The search's text as seen by the survivors (bounds-checked in the instrumented build).
+__device__ __forceinline__ GlobalText global_text(const KParams &p) {
+#if HC_INSTRUMENT
+    return GlobalText{p.y, p.n};
+#else
+    return GlobalText{p.y};
+#endif
+}
 
 // Shared-memory loads by shared-space address.  Not volatile: callers make the
 // address depend on a value produced after the mbarrier wait (see fence_value), so
 // they cannot be hoisted above it.
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
+    chk_shared(a, 8);
     uint64_t r;
     asm("ld.shared.u64 %0, [%1];" : "=l"(r) : "r"(a));
     return r;
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    chk_shared(a, 4);
     uint32_t r;
     asm("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
     return r;
 }
 __device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    chk_shared(a, 1);
     uint32_t r;
     asm("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(a));
     return r;
@@ -883,6 +941,7 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    chk_shared(dst, 16);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }

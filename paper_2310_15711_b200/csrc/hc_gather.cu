@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kGatherThreads, Q <= 4 ? 4 : 3) gather_kernel(
     // the filter bitmap first (its loads must not queue behind the lattice's DRAM misses)
     uint32_t bw = 0;
     if (tid < Lo.bits_words) bw = __ldg(p.Fbits + tid);
-    const GlobalText txt{p.y};
+    const GlobalText txt = global_text(p);
     const uint32_t total_warps = gridDim.x * NW;
     const uint32_t c0 = blockIdx.x * NW + warp;
     const uint32_t L = p.seg_per_chunk / 32;   // lattice points per lane per chunk: 1, 2 or 4

@@ -59,7 +59,7 @@ struct MWarp {   // one warp's per-pattern queues and output state (shared memor
         __syncwarp();
         const KParams &pp = s_params[i];
         const FTable ft{f0 + i * fbytes};
-        const GlobalText gtxt{pp.y};
+        const GlobalText gtxt = global_text(pp);
         WarpOut wo{wbuf_of(i), state[2 * i + 1]};
         WarpQueueSink<Q, SH, GlobalText> sink{pp, gtxt, ft, sx, nullptr, q2_of(i),
                                               0u, state[2 * i], wo, lane, i};
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
         // large shifts: no staging, the lattice q-grams are read from global memory (the
         // gather path's access), hashed once and tested against every pattern: the
         // patterns share the DRAM sectors the lattice touches
-        const GlobalText gtxt{p.y};
+        const GlobalText gtxt = global_text(p);
         for (uint32_t c = gw; c < p.nchunks; c += total_warps) {
             const uint32_t k0 = c * p.seg_per_chunk;
             mstream_filter<Q, SH, GlobalText>(p, gtxt, P, k0, min(k0 + p.seg_per_chunk, p.K), lane, mw,
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KP
     for (uint32_t i = 0; i < P; ++i) {
         const KParams &pp = s_params[i];
         const FTable ft{mw.f0 + i * mw.fbytes};
-        const GlobalText gtxt{pp.y};
+        const GlobalText gtxt = global_text(pp);
         WarpOut wo{mw.wbuf_of(i), mw.state[2 * i + 1]};
         WarpQueueSink<Q, SH, GlobalText> sink{pp, gtxt, ft, sx0 + i * L.x_stride, nullptr,
                                               mw.q2_of(i), 0u, mw.state[2 * i], wo, lane, i};

@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3) staged_kernel(const KParams
                 const SmemText btxt{act ? meta[2 * (b + lane) + 1] : txt.base};
                 run_segments<Q, SH>(p, btxt, sF, sx, act, act ? meta[2 * (b + lane)] : 0u, wo, lane);
             }
-            const GlobalText gtxt{p.y};
+            const GlobalText gtxt = global_text(p);
             for (uint32_t b = 0; b < nm; b += 32) {
                 const bool act = b + lane < nm;
                 run_segments<Q, SH>(p, gtxt, sF, sx, act, act ? mine[b + lane] : 0u, wo, lane);

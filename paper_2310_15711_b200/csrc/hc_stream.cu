@@ -153,6 +153,7 @@ __device__ __forceinline__ void tma_issue(const KParams &p, const TmaStream &ts,
         if (lane == 0) {
             const uintptr_t A = (ts.y + first) & ~static_cast<uintptr_t>(15);
             const uint32_t bytes = (((ts.y32 + first) & 15u) + ts.len + 15u) & ~15u;
+            chk_text_range(p.y, p.n, A, bytes);
             mbar_arrive_expect_tx(&ts.bar[b], bytes);
             bulk_g2s(buf, reinterpret_cast<const void *>(A), bytes, &ts.bar[b]);
         }
@@ -175,6 +176,7 @@ __device__ __forceinline__ void tma_issue(const KParams &p, const TmaStream &ts,
     if (lane == 0) {
         fence_proxy_async();                         // the lanes' stores above
         if (hi > lo) {
+            chk_text_range(p.y, p.n, lo, static_cast<uint32_t>(hi - lo));
             mbar_arrive_expect_tx(&ts.bar[b], static_cast<uint32_t>(hi - lo));
             bulk_g2s(buf + static_cast<uint32_t>(lo - A), reinterpret_cast<const void *>(lo),
                      static_cast<uint32_t>(hi - lo), &ts.bar[b]);
@@ -257,6 +259,7 @@ __device__ __forceinline__ void final_drain_boxes(const KParams &p, const FTable
             for (uintptr_t w = A; w < B; w += 16) {
                 const uint32_t d = box + static_cast<uint32_t>(w - A);
                 if (w >= y && w + 16 <= ye) {
+                    chk_text_range(p.y, p.n, w, 16);
                     cp_async16(d, reinterpret_cast<const void *>(w));
                 } else {
                     for (uint32_t b = 0; b < 16; ++b)
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KPar
     const PassBits pb{fence_value(smem_u32(smem + L.bits_off)) + (p.lane_bits ? 4 * lane : 0u),
                       p.lane_bits ? 7u : 2u};
     WarpOut wo{reinterpret_cast<uint32_t *>(smem + L.wbuf_off) + warp * kWarpBuf, 0u};
-    const GlobalText gtxt{p.y};
+    const GlobalText gtxt = global_text(p);
     WarpQueueSink<Q, SH, GlobalText, FTable> sink{p, gtxt, sF, sx, nullptr,
                                           reinterpret_cast<uint32_t *>(smem + L.q2_off) + warp * kWarpBuf,
                                           0u, 0u, wo, lane};

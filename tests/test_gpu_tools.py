@@ -6,6 +6,8 @@
   parity driver tools/sanitize_case.py (every path against brute force) must FAIL
   with the hook on and pass with it off: the parity check catches a corrupted
   kernel.
+* Bounds-checked build: the instrumented build traps on any text access outside the text
+  or the CTA's shared memory; the parity driver must pass under it.
 * compute-sanitizer: opt-in (HC_SANITIZER=memcheck|racecheck|synccheck), one tool per
   run, because several sanitizer tools in one GPU session are not safe on this pool
   (B200_PROFILING.md); logs of the runs are kept in profiles/.
@@ -41,6 +43,18 @@ def test_fault_injection_is_caught():
     assert "MISMATCH" in red.stdout
     green = _run(["--small"], {"HC_LIB": INSTR})
     assert green.returncode == 0, green.stdout + green.stderr
+
+
+@pytest.mark.skipif(not os.path.exists(INSTR), reason="libhc_instr.so not built")
+def test_bounds_checked_build():
+    """Our own memcheck (compute-sanitizer is closed on this pool): the instrumented build
+    checks every text access (aligned global words must hold a byte of [y, y + n), shared
+    accesses must lie inside the CTA's shared memory, copies must read inside the text) and
+    traps outside.  Every path, aligned and unaligned texts, odd lengths, edge chunks: no
+    trap, every result equal to brute force."""
+    r = _run(["--small", "--unaligned"], {"HC_LIB": INSTR})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    assert "0 mismatches" in r.stdout
 
 
 @pytest.mark.skipif(os.environ.get("HC_SANITIZER") not in ("memcheck", "racecheck", "synccheck"),

@@ -32,6 +32,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--inject", action="store_true", help="fault hook on (instrumented build)")
     ap.add_argument("--small", action="store_true", help="fewer cases (racecheck is slow)")
+    ap.add_argument("--unaligned", action="store_true",
+                    help="also texts at odd offsets / odd lengths and small chunks (edge chunks): "
+                         "with the instrumented build every text access is bounds-checked "
+                         "against [y, y + n) and traps outside it")
     args = ap.parse_args()
     dbg = 9 if args.inject else 0
     rng = np.random.default_rng(91)
@@ -64,6 +68,28 @@ def main():
             if not np.array_equal(got, want):
                 bad += 1
                 print(f"MISMATCH m={len(x)} path={path}: {len(got)} vs {len(want)}", flush=True)
+    if args.unaligned:
+        big = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+        for x, q, a, yy in cases[:5]:
+            for off, cut in ((1, 0), (13, 5), (16, 11)):
+                yv = yy[:len(yy) - cut]
+                want = oracle.brute(x, yv)
+                big[off:off + len(yv)] = torch.from_numpy(yv).cuda()
+                yd = big[off:off + len(yv)]
+                h = hc.prepare(x, q, a)
+                for path, kw in ((hc.PATH_AUTO, {}), (hc.PATH_STREAM, {"tile_bytes": 700, "max_ctas": 3}),
+                                 (hc.PATH_STREAM, {"seg_per_lane": -1, "block_warps": 3}),
+                                 (hc.PATH_GATHER, {"max_ctas": 2}), (hc.PATH_SCAN, {}), (hc.PATH_SHC, {}),
+                                 (hc.PATH_STAGED, {})):
+                    try:
+                        got = hc.search(h, yd, path=path, **kw).cpu().numpy()
+                    except hc.HCError as e:
+                        if e.code == hc.HC_EINVAL and path in (hc.PATH_SHC, hc.PATH_STAGED, hc.PATH_SCAN, hc.PATH_STREAM):
+                            continue
+                        raise
+                    if not np.array_equal(got, want):
+                        bad += 1
+                        print(f"MISMATCH unaligned m={len(x)} off={off} cut={cut} path={path}", flush=True)
     # multi-pattern launches (hc_search_batch)
     xs = [y[o:o + 16].copy() for o in rng.integers(0, n - 16, 4)]
     hb = [hc.prepare(x, 6, 12) for x in xs]
