@@ -101,10 +101,15 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
                 const uint32_t c = __popc(pm);
                 const uint32_t tot = __reduce_add_sync(HC_FULL, c);
                 if (c) {
+                    // one store in the common case (a lane rarely has two passes in a trip)
                     uint32_t slot = atomicAdd(qu.ctr, c);
-#pragma unroll
-                    for (int u = 0; u < kStreamUnroll; ++u)
-                        if ((pm >> u) & 1u) qu.q1[slot++] = pos + u * step;
+                    uint32_t rest = pm;
+#pragma unroll 1
+                    do {
+                        const uint32_t u = __ffs(rest) - 1;
+                        qu.q1[slot++] = pos + u * step;
+                        rest &= rest - 1;
+                    } while (rest);
                 }
                 qu.n1 += tot;
             }
