@@ -21,6 +21,9 @@ LIB = os.path.join(HERE, "libhc.so")
 # instrumented build (HC_INSTRUMENT=1): opts.debug modes and %globaltimer traces compiled
 # in, for tools/ only; the product library rejects them (HC_EINVAL)
 LIB_INSTR = os.path.join(HERE, "libhc_instr.so")
+# bounds-checked build (HC_BOUNDS=1: every text access checked, traps outside; only the few
+# (q, s) instantiations tools/sanitize_case.py uses): tests/test_gpu_tools.py
+LIB_CHK = os.path.join(HERE, "libhc_chk.so")
 OBJ = os.path.join(ROOT, "build_obj")
 SOURCES = ["hc_api.cpp", "hc_launch.cu", "hc_stream.cu", "hc_gather.cu", "hc_mstream.cu",
            "hc_finish.cu", "hc_shc.cu", "hc_staged.cu", "hc_scan.cu"]
@@ -49,6 +52,10 @@ def _compile(src: str, obj: str, defs: list, verbose: bool) -> None:
            "-Xptxas", "-v" if verbose else "-O3", *defs, "-I", INCLUDE, "-I", CSRC,
            "-c", os.path.join(CSRC, src), "-o", obj]
     subprocess.check_call(cmd)
+
+
+def build_bounds_checked(force: bool = False) -> str:
+    return build(force=force, variant="chk", defines=("HC_BOUNDS=1", "HC_FEW_BUILDS=1"))
 
 
 def build(force: bool = False, verbose: bool = False, instrument: bool = False,

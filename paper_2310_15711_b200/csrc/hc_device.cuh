@@ -36,6 +36,12 @@
 #ifndef HC_INSTRUMENT
 #define HC_INSTRUMENT 0
 #endif
+#ifndef HC_BOUNDS
+#define HC_BOUNDS 0      // 1: every text access bounds-checked (libhc_chk.so, tests only)
+#endif
+#ifndef HC_FEW_BUILDS
+#define HC_FEW_BUILDS 0  // 1: only the (q, s) instantiations the bounds-check driver uses
+#endif
 #ifndef HC_LDG_MODE
 #define HC_LDG_MODE 1   // global text words: 0 = ld.global.nc, 1 = + .L2::64B (default: measured
                         // 293 -> 167 MB DRAM read at C2 m = 128), 2 = + L1::no_allocate
@@ -94,11 +100,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void chk_shared(uint32_t a, uint32_t bytes);   // instrumented build
+__device__ __forceinline__ void chk_shared(uint32_t a, uint32_t bytes);   // HC_BOUNDS build
 // 1-D TMA bulk copy global -> shared, completion signalled on `bar` (tx bytes).
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {
-#if HC_INSTRUMENT
+#if HC_BOUNDS
     chk_shared(dst, 16);
     chk_shared(dst + bytes - 16, 16);
     if ((bytes & 15) || (reinterpret_cast<uintptr_t>(src) & 15)) __trap();
@@ -165,21 +171,22 @@ __device__ __forceinline__ uint64_t shl64(uint64_t a, uint32_t s) {
 
 // ------------------------------------------------------------------ text access
 // Text byte p (0 <= p < n) of y, read from global memory (read-only path).
-// Instrumented build: every text access is bounds-checked (compute-sanitizer is closed on
-// this GPU pool, so the memcheck is our own): an aligned global word must hold at least one
-// byte of [y, y + n), a shared access must lie inside the CTA's shared memory, copies into
+// Bounds-checked build (HC_BOUNDS=1, libhc_chk.so; compute-sanitizer is closed on this GPU
+// pool, so the memcheck is our own): an aligned global word must hold at least one byte of
+// [y, y + n), a shared access must lie inside the CTA's dynamic shared memory, copies into
 // shared memory must read inside the text.  A violation traps: the parity driver of
-// tests/test_gpu_tools.py (every path, small inputs, exact-size texts) then fails.
+// tests/test_gpu_tools.py (every path, aligned and unaligned texts) then fails.  The checks
+// cost ~50% of a search, so they are not part of the instrumented (timing) build.
 __device__ __forceinline__ void chk_fail() {
-#if HC_INSTRUMENT
+#if HC_BOUNDS
     __trap();
 #endif
 }
-#if HC_INSTRUMENT
+#if HC_BOUNDS
 extern __shared__ __align__(128) uint8_t hc_chk_dyn_smem[];   // the kernels' dynamic shared memory
 #endif
 __device__ __forceinline__ void chk_shared(uint32_t a, uint32_t bytes) {
-#if HC_INSTRUMENT
+#if HC_BOUNDS
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     const uint32_t lo = static_cast<uint32_t>(__cvta_generic_to_shared(hc_chk_dyn_smem));
@@ -187,13 +194,13 @@ __device__ __forceinline__ void chk_shared(uint32_t a, uint32_t bytes) {
 #endif
 }
 __device__ __forceinline__ void chk_text_range(const uint8_t *y, uint32_t n, uintptr_t a, uint32_t bytes) {
-#if HC_INSTRUMENT
+#if HC_BOUNDS
     if (a < reinterpret_cast<uintptr_t>(y) || a + bytes > reinterpret_cast<uintptr_t>(y) + n) chk_fail();
 #endif
 }
 struct GlobalText {
     const uint8_t *y;
-#if HC_INSTRUMENT
+#if HC_BOUNDS
     uint32_t n = 0;   // text length: accesses are checked when set
     __device__ __forceinline__ void chk(uintptr_t a, uint32_t bytes) const {
         const uintptr_t y0 = reinterpret_cast<uintptr_t>(y);
@@ -239,7 +246,7 @@ struct GlobalText {
 
 // The search's text as seen by the survivors (bounds-checked in the instrumented build).
 __device__ __forceinline__ GlobalText global_text(const KParams &p) {
-#if HC_INSTRUMENT
+#if HC_BOUNDS
     return GlobalText{p.y, p.n};
 #else
     return GlobalText{p.y};
@@ -1266,6 +1273,9 @@ static typename Pick<1, 0>::Fn pick(uint32_t q, uint32_t s) {
 #define HC_C(Q, SH) \
     if (q == Q && s == SH) return Pick<Q, SH>::fn();
     if (q == 1) return Pick<1, 0>::fn();
+#if HC_FEW_BUILDS
+    HC_C(2, 4) HC_C(2, 5) HC_C(3, 3) HC_C(4, 3) HC_C(6, 2) HC_C(8, 1)
+#else
     HC_C(2, 0) HC_C(2, 1) HC_C(2, 2) HC_C(2, 3) HC_C(2, 4) HC_C(2, 5) HC_C(2, 6) HC_C(2, 7)
     HC_C(3, 0) HC_C(3, 1) HC_C(3, 2) HC_C(3, 3) HC_C(3, 4) HC_C(3, 5)
     HC_C(4, 0) HC_C(4, 1) HC_C(4, 2) HC_C(4, 3)
@@ -1273,6 +1283,7 @@ static typename Pick<1, 0>::Fn pick(uint32_t q, uint32_t s) {
     HC_C(6, 0) HC_C(6, 1) HC_C(6, 2)
     HC_C(7, 0) HC_C(7, 1) HC_C(7, 2)
     HC_C(8, 0) HC_C(8, 1)
+#endif
 #undef HC_C
     return nullptr;
 }

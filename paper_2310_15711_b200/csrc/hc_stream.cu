@@ -83,20 +83,11 @@ __device__ __forceinline__ void stream_filter(const KParams &p, const SmemText &
             uint64_t W[kStreamUnroll];
 #pragma unroll
             for (int u = 0; u < kStreamUnroll; ++u) W[u] = end8<Q>(txt, pos + u * step);
-            if (kInstrument && p.debug == 14)          // no text loads (measurement)
-#pragma unroll
-                for (int u = 0; u < kStreamUnroll; ++u) W[u] = (pos + u * step) * 0x9E3779B97F4A7C15ull;
             uint32_t pm = 0;
-            if (kInstrument && p.debug == 13) {        // no F lookups (measurement)
 #pragma unroll
-                for (int u = 0; u < kStreamUnroll; ++u)
-                    pm |= static_cast<uint32_t>(qhash<Q, SH>(W[u], p.mask) == 0xfffffu) << u;
-            } else {
-#pragma unroll
-                for (int u = 0; u < kStreamUnroll; ++u)
-                    pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
-            }
-            if (kInstrument && (p.debug == 3 || p.debug == 14)) pm = 0;   // phase A alone (measurement)
+            for (int u = 0; u < kStreamUnroll; ++u)
+                pm |= static_cast<uint32_t>(sF.pass(qhash<Q, SH>(W[u], p.mask))) << u;
+            if (kInstrument && p.debug == 3) pm = 0;   // phase A alone (measurement)
             if (__any_sync(HC_FULL, pm != 0)) {
                 const uint32_t c = __popc(pm);
                 const uint32_t tot = __reduce_add_sync(HC_FULL, c);

@@ -6,7 +6,7 @@
   parity driver tools/sanitize_case.py (every path against brute force) must FAIL
   with the hook on and pass with it off: the parity check catches a corrupted
   kernel.
-* Bounds-checked build: the instrumented build traps on any text access outside the text
+* Bounds-checked build (libhc_chk.so, HC_BOUNDS=1): traps on any text access outside the text
   or the CTA's shared memory; the parity driver must pass under it.
 * compute-sanitizer: opt-in (HC_SANITIZER=memcheck|racecheck|synccheck), one tool per
   run, because several sanitizer tools in one GPU session are not safe on this pool
@@ -27,6 +27,7 @@ if not torch.cuda.is_available():
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASE = os.path.join(ROOT, "tools", "sanitize_case.py")
 INSTR = os.path.join(ROOT, "paper_2310_15711_b200", "libhc_instr.so")
+CHK = os.path.join(ROOT, "paper_2310_15711_b200", "libhc_chk.so")
 
 
 def _run(args, env_extra=None, prefix=(), timeout=900):
@@ -45,14 +46,14 @@ def test_fault_injection_is_caught():
     assert green.returncode == 0, green.stdout + green.stderr
 
 
-@pytest.mark.skipif(not os.path.exists(INSTR), reason="libhc_instr.so not built")
+@pytest.mark.skipif(not os.path.exists(CHK), reason="libhc_chk.so not built")
 def test_bounds_checked_build():
-    """Our own memcheck (compute-sanitizer is closed on this pool): the instrumented build
-    checks every text access (aligned global words must hold a byte of [y, y + n), shared
+    """Our own memcheck (compute-sanitizer is closed on this pool): the bounds-checked build
+    (HC_BOUNDS=1) checks every text access (aligned global words must hold a byte of [y, y + n), shared
     accesses must lie inside the CTA's shared memory, copies must read inside the text) and
     traps outside.  Every path, aligned and unaligned texts, odd lengths, edge chunks: no
     trap, every result equal to brute force."""
-    r = _run(["--small", "--unaligned"], {"HC_LIB": INSTR})
+    r = _run(["--small", "--unaligned"], {"HC_LIB": CHK})
     assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
     assert "0 mismatches" in r.stdout
 
