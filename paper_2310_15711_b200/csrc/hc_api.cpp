@@ -240,7 +240,8 @@ constexpr uint32_t kDefaultStages = 2;
 constexpr uint32_t kStagedSmem3 = 233472 / 3 - 1024 - 1280;
 constexpr uint32_t kDefaultChunkBytes = 3072;   // stream path: text bytes per warp chunk
 constexpr uint32_t kDefaultStreamBufs = 2;      // stream path: buffers per warp
-constexpr uint32_t kDefaultStreamWarps = 24;    // stream path: warps per CTA (one CTA per SM)
+constexpr uint32_t kDefaultStreamWarps = hc::kStreamFatThreads / 32;   // stream path: most warps per CTA (one CTA per SM)
+constexpr uint32_t kDenseShift = 8;   // up to this shift 24 warps at 85 registers, above 20 warps at 96 (hc_stream.cu)
 constexpr uint32_t kShcLaneBytes = 128;         // SHC path: text bytes per lane and chunk
 // hc_search_batch: patterns of equal (m, q, alpha) with shifts up to this share one
 // streamed pass over the text (multi-pattern stream kernel)
@@ -349,13 +350,14 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
         // 24 warps' chunk buffers.  Fewer warps when the buffers do not fit; the filter bitmap
         // unreplicated (lane_bits = 0) when even 8 warps do not fit beside the replicas.
         p.lane_bits = 1;
-        if (o.block_warps >= 1 && o.block_warps <= 24) {
+        if (o.block_warps >= 1 && o.block_warps <= static_cast<int>(kDefaultStreamWarps)) {
             p.block_warps = static_cast<uint32_t>(o.block_warps);
             if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 1) >
                 smem_budget(h->device))
                 p.lane_bits = 0;
         } else {
-            p.block_warps = kDefaultStreamWarps;
+            const uint32_t w0 = S <= kDenseShift ? kDefaultStreamWarps : hc::kStreamRegThreads / 32;
+            p.block_warps = w0;
             while (p.block_warps > 8 &&
                    hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 1) >
                        smem_budget(h->device))
@@ -363,7 +365,7 @@ int setup_search(const hc_handle *h, const uint8_t *y_dev, uint32_t nn, const hc
             if (hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 1) >
                 smem_budget(h->device)) {
                 p.lane_bits = 0;
-                p.block_warps = kDefaultStreamWarps;
+                p.block_warps = w0;
                 while (p.block_warps > 8 &&
                        hc::stream_smem_bytes(p.alpha, m, p.stage_bytes, p.stages, p.block_warps, 0) >
                            smem_budget(h->device))

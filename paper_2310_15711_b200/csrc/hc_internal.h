@@ -121,7 +121,8 @@ int stream_smem_bytes(uint32_t alpha, uint32_t m, uint32_t buf_bytes, uint32_t b
 constexpr int kStagedThreads = 256;
 constexpr int kGatherThreads = 256;
 constexpr int kStreamMaxThreads = 256;   // SHC and (x2) multi-pattern kernels
-constexpr int kStreamFatThreads = 768;   // stream kernel: one CTA per SM, up to 24 warps
+constexpr int kStreamFatThreads = 768;   // stream kernel: one CTA per SM, up to 24 warps (<= 85 registers)
+constexpr int kStreamRegThreads = 640;   // ... or up to 20 warps with <= 102 registers
 constexpr int kWarpBuf = 64;  // per-warp match buffer entries (shared memory)
 
 }  // namespace hc

@@ -343,13 +343,9 @@ __device__ __forceinline__ void stream_load_tables(const KParams &p, uint32_t *b
     }
 }
 
+// The kernel body; two entry points compile it for two register budgets (below).
 template <int Q, int SH>
-#ifndef HC_STREAM_MINB
-#define HC_STREAM_MINB 3
-#endif
-// One CTA of up to 24 warps per SM (F and the per-lane filter bitmaps are held once per SM):
-// up to 85 registers, no spills in the filter loop (at 64 the loop spilled ~600 B per thread)
-__global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KParams p) {
+__device__ __forceinline__ void stream_body(const KParams &p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t NW = blockDim.x / 32;
     const StreamLayout L = stream_layout(p.alpha, p.m, NW, p.stage_bytes, p.stages, p.lane_bits);
@@ -414,17 +410,38 @@ cudaError_t read_epi_ts(unsigned long long *host8) {   // debug 10 (this TU's st
 }
 #endif
 
+// One CTA per SM (F and the per-lane filter bitmaps are held once per SM), two builds:
+//  - up to 24 warps at <= 85 registers (12 B of spills): dense lattices, S <= 8, where the
+//    filter loop is issue-bound and every warp counts (C2 m = 8, C3/C4 m <= 8: 2-3.5%
+//    faster than the other build);
+//  - up to 20 warps at <= 102 registers (96 used, no spills): every other shift (C2 m = 16
+//    and 32 3.5% faster, C3/C4 m = 16 7%: A/B).
+template <int Q, int SH>
+__global__ void __launch_bounds__(kStreamFatThreads, 1) stream_kernel(const KParams p) {
+    stream_body<Q, SH>(p);
+}
+template <int Q, int SH>
+__global__ void __launch_bounds__(kStreamRegThreads, 1) stream_kernel_r(const KParams p) {
+    stream_body<Q, SH>(p);
+}
+
 template <int Q, int SH>
 struct PickStream {
     using Fn = KernFn;
     static KernFn fn() { return stream_kernel<Q, SH>; }
 };
+template <int Q, int SH>
+struct PickStreamR {
+    using Fn = KernFn;
+    static KernFn fn() { return stream_kernel_r<Q, SH>; }
+};
 
 cudaError_t launch_stream(const KParams &p, cudaStream_t st, int max_ctas, int ctas_per_sm,
                           LaunchInfo *li) {
-    KernFn kern = pick<PickStream>(p.q, p.s);
-    if (!kern) return cudaErrorInvalidValue;
     const uint32_t nw = p.block_warps;
+    KernFn kern = 32 * nw <= static_cast<uint32_t>(kStreamRegThreads) ? pick<PickStreamR>(p.q, p.s)
+                                                                       : pick<PickStream>(p.q, p.s);
+    if (!kern) return cudaErrorInvalidValue;
     const int smem = stream_smem_bytes(p.alpha, p.m, p.stage_bytes, p.stages, nw, p.lane_bits);
     const long ctas = (p.nchunks + nw - 1) / nw;
     KParams a = p;
