@@ -158,7 +158,9 @@ __device__ __forceinline__ void mstream_loop(const KParams &p, uint32_t P, const
 }
 
 template <int Q, int SH>
-__global__ void __launch_bounds__(2 * kStreamMaxThreads) mstream_kernel(const KParams p, const MParams mp) {
+// Shared memory limits this kernel to <= 512 threads per SM (one 16-warp CTA, or two 8-warp
+// CTAs), so it may use up to 128 registers: at the default 64 it spilled 260 B per thread.
+__global__ void __launch_bounds__(2 * kStreamMaxThreads, 1) mstream_kernel(const KParams p, const MParams mp) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t NW = blockDim.x / 32;
     const uint32_t P = mp.npat;
